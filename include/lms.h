@@ -1,0 +1,177 @@
+/*
+ * liblms.so — C ABI of the B200 executor runtime for TFLMS-style swapping.
+ *
+ * The reference package (swapgraph) has no FFI: its executor and its
+ * transfer/memory model are Python functions.  This header is the boundary
+ * that replaces them; every entry point names the reference behaviour it
+ * implements:
+ *
+ *   device pool      <- residency/refcount model, sim.py:116-124, :193-211,
+ *                       :356-401 (alloc at op start, free at refcount 0 AND
+ *                       after outbound transfers, sim.py:205-211, :379-386);
+ *                       capacity/OOM, sim.py:49, :471
+ *   host pool        <- host residency of swapped tensors, sim.py:193-199
+ *   swap_out/in      <- swap node semantics: identity on values
+ *                       (interp.py:168-170) realised as D2H/H2D transfers on
+ *                       per-direction channels (sim.py:284-322); the swap-in
+ *                       is gated by its control edge (rewriter.py:455-477,
+ *                       control.py:158-169)
+ *   stats / trace    <- SimReport / TraceEvent schema, sim.py:74-113
+ *
+ * Conventions: functions return 0 on success and a negative LMS_E* code on
+ * failure; lms_last_error() gives the message (thread-local).  Nothing
+ * throws across the ABI.  Pointers are plain device / host pointers,
+ * streams and events are CUDA runtime handles passed as void*.
+ * The four allocator hooks at the bottom have exactly the signatures of
+ * PyTorch's CUDAPluggableAllocator (torch/csrc/cuda/CUDAPluggableAllocator.h:
+ * alloc_fn(size_t, int, cudaStream_t), free_fn(void*, size_t, int,
+ * cudaStream_t)).
+ */
+#ifndef LMS_H_
+#define LMS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMS_MAX_DIMS 8
+
+enum {
+  LMS_OK = 0,
+  LMS_E_INVALID = -1,   /* bad argument (ValueError in the Python wrapper) */
+  LMS_E_OOM = -2,       /* device budget exceeded (SimReport.oom analogue) */
+  LMS_E_HOST_OOM = -3,  /* pinned host pool cannot grow */
+  LMS_E_CUDA = -4,      /* CUDA runtime error; message has the details */
+  LMS_E_STATE = -5      /* call out of order (e.g. swap_in of a released handle) */
+};
+
+/* Transfer codecs for swap-out.  RAW_CE moves the tensor's storage span with
+ * the copy engine (packing first only when the view is not dense).  RAW_SM
+ * moves it with an SM kernel writing straight into mapped pinned memory
+ * (fused pack for strided views).  ZVC is lossless zero-value compression:
+ * an SM kernel writes a bitmask plus the nonzero words into pinned memory,
+ * and the swap-in decodes after a copy-engine H2D of the compressed bytes. */
+enum { LMS_CODEC_RAW_CE = 0, LMS_CODEC_RAW_SM = 1, LMS_CODEC_ZVC = 2 };
+
+typedef struct lms_ctx lms_ctx;
+typedef struct lms_handle lms_handle;
+
+typedef struct {
+  int device;                 /* CUDA ordinal */
+  size_t device_reserve;      /* bytes reserved for the device arena (0 = none yet) */
+  size_t device_limit;        /* enforced budget in bytes (0 = arena size) */
+  size_t host_reserve;        /* pinned bytes to pre-allocate */
+  size_t host_chunk;          /* growth granularity of the pinned pool */
+  int overlap_transfers;      /* 1: separate D2H/H2D streams (sim.py:287-290) */
+  int timing;                 /* 1: record per-transfer timing events */
+  int sm_ctas;                /* CTAs for SM-driven transfer/codec kernels (0 = auto) */
+} lms_config_t;
+
+typedef struct {
+  uint64_t device_in_use, device_peak, device_reserved, device_limit;
+  uint64_t device_largest_free, device_deferred_bytes;
+  uint64_t host_in_use, host_peak, host_reserved;
+  uint64_t n_alloc, n_free, n_oom, n_deferred_frees, n_cross_stream_waits;
+  uint64_t n_swap_out, n_swap_in, n_handles_live;
+  uint64_t d2h_logical_bytes, d2h_wire_bytes;   /* tensor bytes vs bytes on PCIe */
+  uint64_t h2d_logical_bytes, h2d_wire_bytes;
+  uint64_t kernel_launches;                     /* our sm_100a kernels */
+  double d2h_busy_ms, h2d_busy_ms;              /* sum of transfer spans (timing=1) */
+  double swap_wait_ms;  /* consumer stalls on swap-ins (timing=1): transfer_wait_total */
+} lms_stats_t;
+
+/* one measured transfer, in the TraceEvent vocabulary (sim.py:74-81) */
+typedef struct {
+  int64_t handle_id;
+  int direction;        /* 0 = D2H (swap-out), 1 = H2D (swap-in) */
+  int codec;
+  uint64_t logical_bytes, wire_bytes;
+  double start_ms, end_ms;   /* relative to the context epoch */
+} lms_xfer_record_t;
+
+const char* lms_last_error(void);
+const char* lms_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+int lms_default_config(lms_config_t* cfg);
+int lms_create(const lms_config_t* cfg, lms_ctx** out);
+int lms_destroy(lms_ctx* ctx);
+/* The context the allocator hooks below use (one per process / device). */
+int lms_set_global(lms_ctx* ctx);
+lms_ctx* lms_get_global(void);
+/* Stream that owns freed blocks for immediate reuse (torch's compute stream). */
+int lms_set_home_stream(lms_ctx* ctx, void* stream);
+int lms_set_limit(lms_ctx* ctx, size_t limit);
+int lms_reset_peaks(lms_ctx* ctx);
+int lms_get_streams(lms_ctx* ctx, void** d2h, void** h2d);
+
+/* ---- device pool (replaces the simulator's residency model) ------------- */
+int lms_dev_alloc(lms_ctx* ctx, size_t size, void* stream, void** out);
+int lms_dev_free(lms_ctx* ctx, void* ptr, void* stream);
+/* keep the block containing ptr from reuse until the work now enqueued on
+ * `stream` completes (a pending outbound transfer), like sim.py:205-211
+ * "free after transfers done" */
+int lms_dev_hold_until(lms_ctx* ctx, const void* ptr, void* stream);
+/* storage layout the swap-in restores by default: strides (elements) and the
+ * number of storage elements to allocate */
+int lms_handle_layout(lms_handle* h, int64_t* strides_out, int64_t* storage_elems);
+
+/* ---- host pool ------------------------------------------------------------ */
+int lms_host_alloc(lms_ctx* ctx, size_t size, void** out);
+int lms_host_free(lms_ctx* ctx, void* ptr);
+
+/* ---- swap engine ------------------------------------------------------------ */
+/* Swap-out: the D2H channel waits for the work already enqueued on
+ * `producer_stream`, then moves the tensor (sizes/strides in elements) to
+ * pinned memory with `codec`.  The source block is held until the transfer
+ * completes, so freeing it right away is safe. */
+int lms_swap_out(lms_ctx* ctx, const void* src, const int64_t* sizes, const int64_t* strides,
+                 int ndim, int elem_size, void* producer_stream, int codec, lms_handle** out);
+/* Swap-in: the H2D channel waits for the work already enqueued on
+ * `trigger_stream` (the control op's completion point) and for the swap-out,
+ * then restores the values into `dst` (layout `dst_strides`, or contiguous
+ * when NULL). */
+int lms_swap_in(lms_ctx* ctx, lms_handle* h, void* dst, const int64_t* dst_strides,
+                void* trigger_stream);
+/* Make `consumer_stream` wait until the last swap-in of `h` has landed. */
+int lms_swap_wait(lms_ctx* ctx, lms_handle* h, void* consumer_stream);
+/* Host-side query: 1 if the swap-out finished, 0 if still in flight. */
+int lms_swap_out_done(lms_ctx* ctx, lms_handle* h);
+/* Release the host copy (deferred until pending H2D reads finish). */
+int lms_handle_release(lms_ctx* ctx, lms_handle* h);
+int lms_handle_info(lms_handle* h, int64_t* id, uint64_t* logical_bytes, uint64_t* wire_bytes,
+                    int* codec);
+
+/* ---- staging kernels (sm_100a), usable on their own ------------------------ */
+/* dst (contiguous) <- src (strided view) */
+int lms_pack(lms_ctx* ctx, void* dst, const void* src, const int64_t* sizes,
+             const int64_t* strides, int ndim, int elem_size, void* stream);
+/* dst (strided view) <- src (contiguous) */
+int lms_unpack(lms_ctx* ctx, void* dst, const void* src, const int64_t* sizes,
+               const int64_t* strides, int ndim, int elem_size, void* stream);
+/* ZVC codec over `nwords` 32-bit words; encode writes to any device-visible
+ * buffer (pinned host included) of at least lms_zvc_bound(nwords) bytes. */
+size_t lms_zvc_bound(size_t nwords);
+int lms_zvc_encode(lms_ctx* ctx, const void* src, size_t nwords, void* dst, void* stream);
+int lms_zvc_decode(lms_ctx* ctx, const void* enc, size_t nwords, void* dst, void* stream);
+/* bytes used by an encoded stream whose header is host-readable */
+int lms_zvc_encoded_size(const void* enc_host, size_t* out);
+
+/* ---- stats / trace -------------------------------------------------------- */
+int lms_stats(lms_ctx* ctx, lms_stats_t* out);
+/* copies up to `cap` finished transfer records; returns count via *n */
+int lms_trace(lms_ctx* ctx, lms_xfer_record_t* out, size_t cap, size_t* n);
+int lms_trace_clear(lms_ctx* ctx);
+int lms_synchronize(lms_ctx* ctx);
+
+/* ---- PyTorch CUDAPluggableAllocator hooks (use the global context) -------- */
+void* lms_alloc(size_t size, int device, void* stream);
+void lms_free(void* ptr, size_t size, int device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMS_H_ */

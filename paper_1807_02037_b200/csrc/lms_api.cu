@@ -1,0 +1,1086 @@
+// liblms.so: device pool, pinned host pool and swap engine behind the C ABI
+// declared in include/lms.h.  See that header for the reference semantics
+// each entry point implements.
+//
+// Streams: each context owns one D2H and one H2D stream (the simulator's
+// per-direction channels, sim.py:284-322); with overlap_transfers=0 both
+// directions share one stream (the shared "xfer" channel, sim.py:287-290).
+// The compute stream belongs to the caller (PyTorch's current stream).
+//
+// Device blocks are tagged with the stream that last used them.  A block is
+// handed to another stream only after that stream waits on an event
+// recorded on the previous owner, and a block read by an in-flight swap-out
+// is not reused before the copy completes (sim.py:205-211).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/lms.h"
+#include "arena.h"
+#include "kernels.cuh"
+
+namespace lms {
+
+static thread_local std::string g_err;
+static lms_ctx* g_global = nullptr;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                     \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return fail(LMS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+static void* const kFresh = reinterpret_cast<void*>(~uintptr_t(0));
+
+struct OomError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ---------------------------------------------------------------------------
+// events: disable-timing events recycled through a free list
+
+class EventPool {
+ public:
+  cudaEvent_t get(bool timing = false) {
+    auto& fl = timing ? timed_ : plain_;
+    if (!fl.empty()) {
+      cudaEvent_t e = fl.back();
+      fl.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+    return e;
+  }
+  void put(cudaEvent_t e, bool timing = false) {
+    if (e) (timing ? timed_ : plain_).push_back(e);
+  }
+  ~EventPool() {
+    for (auto e : plain_) cudaEventDestroy(e);
+    for (auto e : timed_) cudaEventDestroy(e);
+  }
+
+ private:
+  std::vector<cudaEvent_t> plain_, timed_;
+};
+
+// shared, reference-counted event (one swap-out event may hold a block and
+// gate several swap-ins)
+struct SharedEv {
+  cudaEvent_t e = nullptr;
+  int refs = 0;
+};
+
+struct XferRec {
+  int64_t handle_id;
+  int direction, codec;
+  uint64_t logical, wire;
+  cudaEvent_t start, end;
+};
+
+}  // namespace lms
+
+using namespace lms;
+
+struct lms_handle {
+  int64_t id = 0;
+  int ndim = 0;
+  int64_t sizes[LMS_MAX_DIMS] = {};
+  int64_t strides[LMS_MAX_DIMS] = {};
+  int elem = 0;
+  int64_t numel = 0;
+  int64_t span = 0;        // storage elements covered by the view
+  bool packed = false;     // host copy is contiguous (view was not dense)
+  int codec = LMS_CODEC_RAW_CE;
+  char* host = nullptr;
+  size_t host_bytes = 0;   // reserved
+  uint64_t logical = 0;    // tensor bytes
+  uint64_t wire = 0;       // bytes that crossed PCIe on swap-out (bound until known)
+  SharedEv* out_done = nullptr;
+  cudaEvent_t in_ready = nullptr;  // last swap-in (H2D is in order: covers all reads)
+  bool wire_known = true;          // false until a ZVC header has been read back
+  int64_t rec_out = -1;            // index of the swap-out timing record
+  int64_t rec_in = -1;             // index of the last swap-in timing record
+  bool released = false;
+};
+
+struct lms_ctx {
+  lms_config_t cfg{};
+  std::mutex mu;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t d2h = nullptr, h2d = nullptr;
+  void* home = nullptr;  // compute stream (immediate reuse)
+  EventPool events;
+
+  // device arena
+  char* dev_base = nullptr;
+  Arena dev;
+  size_t limit = 0;
+  std::unordered_map<Block*, std::vector<SharedEv*>> holds;
+  std::vector<Block*> deferred;
+  size_t deferred_bytes = 0;
+
+  // pinned host pool: chunks, each an arena
+  struct Chunk {
+    char* base;
+    Arena* arena;
+  };
+  std::vector<Chunk> chunks;
+  size_t host_reserved = 0;
+  size_t host_used = 0, host_peak = 0;
+  std::vector<lms_handle*> zombie;   // released handles waiting for H2D reads
+  std::vector<lms_handle*> zvc_open; // ZVC swap-outs whose compressed size is not yet known
+
+  // ZVC scratch on the D2H stream
+  uint32_t* zvc_scratch = nullptr;
+  size_t zvc_scratch_words = 0;
+
+  // stats
+  lms_stats_t st{};
+  int64_t next_id = 1;
+
+  // timing
+  cudaEvent_t epoch = nullptr;
+  std::vector<XferRec> recs;
+  // consumer reached its wait (event on the consumer stream) vs swap-in record
+  std::vector<std::pair<cudaEvent_t, int64_t>> waits;
+};
+
+namespace {
+
+// -------------------------------------------------------------------------
+// device pool internals (caller holds ctx->mu)
+
+void retire_event(lms_ctx* c, SharedEv* ev) {
+  if (--ev->refs == 0) {
+    c->events.put(ev->e);
+    delete ev;
+  }
+}
+
+// drop completed holds; true if the block has none left
+bool holds_clear(lms_ctx* c, Block* b) {
+  auto it = c->holds.find(b);
+  if (it == c->holds.end()) return true;
+  auto& v = it->second;
+  size_t w = 0;
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (cudaEventQuery(v[i]->e) == cudaSuccess) retire_event(c, v[i]);
+    else v[w++] = v[i];
+  }
+  v.resize(w);
+  if (w == 0) {
+    c->holds.erase(it);
+    return true;
+  }
+  return false;
+}
+
+void reap_deferred(lms_ctx* c, bool block) {
+  size_t w = 0;
+  for (size_t i = 0; i < c->deferred.size(); ++i) {
+    Block* b = c->deferred[i];
+    if (block) {
+      auto it = c->holds.find(b);
+      if (it != c->holds.end())
+        for (auto* ev : it->second) cudaEventSynchronize(ev->e);
+    }
+    if (holds_clear(c, b)) {
+      c->deferred_bytes -= b->size;
+      c->dev.release(b);
+    } else {
+      c->deferred[w++] = b;
+    }
+  }
+  c->deferred.resize(w);
+}
+
+void stream_wait_on(lms_ctx* c, void* waiter, void* owner) {
+  cudaEvent_t e = c->events.get();
+  cudaEventRecord(e, static_cast<cudaStream_t>(owner));
+  cudaStreamWaitEvent(static_cast<cudaStream_t>(waiter), e, 0);
+  c->events.put(e);  // recycled after the wait is enqueued: safe, re-record only later
+  c->st.n_cross_stream_waits++;
+}
+
+int ensure_arena(lms_ctx* c) {
+  if (c->dev_base) return LMS_OK;
+  size_t want = c->cfg.device_reserve;
+  if (want == 0) {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    want = fr > (size_t(2) << 30) ? fr - (size_t(2) << 30) : fr / 2;
+    if (c->cfg.device_limit && c->cfg.device_limit < want) want = c->cfg.device_limit;
+  }
+  void* p = nullptr;
+  CK(cudaMalloc(&p, want));
+  c->dev_base = static_cast<char*>(p);
+  c->dev.init(c->dev_base, want, kFresh);
+  if (c->limit == 0 || c->limit > c->dev.capacity()) c->limit = c->dev.capacity();
+  return LMS_OK;
+}
+
+// returns LMS_OK and *out, or LMS_E_OOM
+int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
+  int rc = ensure_arena(c);
+  if (rc) return rc;
+  size_t need = Arena::round(size);
+  reap_deferred(c, false);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if (c->dev.used() + need <= c->limit) {
+      Block* b = c->dev.alloc(need, stream);
+      if (b) {
+        void* prev = b->tag;
+        if (prev != kFresh && prev != stream) stream_wait_on(c, stream, prev);
+        b->tag = stream;
+        c->st.n_alloc++;
+        *out = c->dev_base + b->off;
+        return LMS_OK;
+      }
+    }
+    if (attempt == 0) {
+      if (c->deferred.empty()) attempt = 1; else reap_deferred(c, true);
+    }
+    if (attempt == 1) {
+      // merge blocks split by stream tags: after a device sync nothing is pending
+      cudaDeviceSynchronize();
+      reap_deferred(c, true);
+      std::vector<Block*> fr;
+      c->dev.for_each_free([&](Block* b) { if (b->tag != kFresh) fr.push_back(b); });
+      for (Block* b : fr) {
+        if (b->free) c->dev.retag_free(b, kFresh);
+      }
+    }
+  }
+  c->st.n_oom++;
+  char buf[256];
+  snprintf(buf, sizeof buf,
+           "LMS_OOM: device budget exhausted allocating %zu bytes (in use %zu, limit %zu, "
+           "largest free block %zu)", size, c->dev.used(), c->limit, c->dev.largest_free());
+  return fail(LMS_E_OOM, buf);
+}
+
+int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
+  if (!ptr) return LMS_OK;
+  if (!c->dev.owns(ptr)) return fail(LMS_E_INVALID, "lms_dev_free: pointer not from the device pool");
+  Block* b = c->dev.find_live(static_cast<char*>(ptr) - c->dev_base);
+  if (!b) return fail(LMS_E_INVALID, "lms_dev_free: not a live allocation");
+  b->tag = stream;
+  c->st.n_free++;
+  if (!holds_clear(c, b)) {
+    c->deferred.push_back(b);
+    c->deferred_bytes += b->size;
+    c->st.n_deferred_frees++;
+    return LMS_OK;
+  }
+  c->dev.release(b);
+  return LMS_OK;
+}
+
+// -------------------------------------------------------------------------
+// host pool internals (caller holds ctx->mu)
+
+int host_alloc_locked(lms_ctx* c, size_t size, void** out) {
+  size_t need = Arena::round(size);
+  for (auto& ch : c->chunks) {
+    Block* b = ch.arena->alloc(need);
+    if (b) {
+      *out = ch.base + b->off;
+      c->host_used += b->size;
+      c->host_peak = std::max(c->host_peak, c->host_used);
+      return LMS_OK;
+    }
+  }
+  size_t grow = std::max(need, c->cfg.host_chunk ? c->cfg.host_chunk : (size_t(1) << 30));
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, grow, cudaHostAllocPortable | cudaHostAllocMapped);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LMS_E_HOST_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+  }
+  auto* a = new Arena();
+  a->init(static_cast<char*>(p), grow);
+  c->chunks.push_back({static_cast<char*>(p), a});
+  c->host_reserved += grow;
+  Block* b = a->alloc(need);
+  *out = static_cast<char*>(p) + b->off;
+  c->host_used += b->size;
+  c->host_peak = std::max(c->host_peak, c->host_used);
+  return LMS_OK;
+}
+
+int host_free_locked(lms_ctx* c, void* ptr) {
+  for (auto& ch : c->chunks) {
+    if (ch.arena->owns(ptr)) {
+      Block* b = ch.arena->find_live(static_cast<char*>(ptr) - ch.base);
+      if (!b) return fail(LMS_E_INVALID, "lms_host_free: not a live allocation");
+      c->host_used -= b->size;
+      ch.arena->release(b);
+      return LMS_OK;
+    }
+  }
+  return fail(LMS_E_INVALID, "lms_host_free: pointer not from the host pool");
+}
+
+// learn the compressed size of finished ZVC swap-outs (header in pinned memory)
+void account_zvc(lms_ctx* c) {
+  size_t w = 0;
+  for (size_t i = 0; i < c->zvc_open.size(); ++i) {
+    lms_handle* h = c->zvc_open[i];
+    if (cudaEventQuery(h->out_done->e) != cudaSuccess) {
+      c->zvc_open[w++] = h;
+      continue;
+    }
+    const ZvcHeader* hd = reinterpret_cast<const ZvcHeader*>(h->host);
+    h->wire = hd->magic == kZvcMagic ? hd->bytes : h->host_bytes;
+    h->wire_known = true;
+    c->st.d2h_wire_bytes += h->wire;
+    if (h->rec_out >= 0 && size_t(h->rec_out) < c->recs.size()) c->recs[h->rec_out].wire = h->wire;
+  }
+  c->zvc_open.resize(w);
+}
+
+void reap_zombies(lms_ctx* c) {
+  account_zvc(c);
+  size_t w = 0;
+  for (size_t i = 0; i < c->zombie.size(); ++i) {
+    lms_handle* h = c->zombie[i];
+    bool busy = h->in_ready && cudaEventQuery(h->in_ready) != cudaSuccess;
+    if (h->out_done && cudaEventQuery(h->out_done->e) != cudaSuccess) busy = true;
+    if (busy || !h->wire_known) {
+      c->zombie[w++] = h;
+      continue;
+    }
+    if (h->out_done) retire_event(c, h->out_done);
+    if (h->in_ready) c->events.put(h->in_ready);
+    if (h->host) host_free_locked(c, h->host);
+    delete h;
+  }
+  c->zombie.resize(w);
+}
+
+// -------------------------------------------------------------------------
+// launch helpers
+
+int sm_grid(lms_ctx* c, int64_t work_items, int per_cta) {
+  int64_t want = (work_items + per_cta - 1) / per_cta;
+  int cap = c->cfg.sm_ctas > 0 ? c->cfg.sm_ctas : c->num_sms * 4;
+  if (want < 1) want = 1;
+  return int(std::min<int64_t>(want, cap));
+}
+
+bool dense_layout(int ndim, const int64_t* sizes, const int64_t* strides, int64_t* span_out,
+                  int64_t* numel_out) {
+  int64_t numel = 1, span = 1;
+  for (int k = 0; k < ndim; ++k) {
+    numel *= sizes[k];
+    if (sizes[k] > 1) span += (sizes[k] - 1) * strides[k];
+  }
+  if (numel == 0) span = 0;
+  *span_out = span;
+  *numel_out = numel;
+  return span <= numel;
+}
+
+void to_desc(Strided* d, int ndim, const int64_t* sizes, const int64_t* strides) {
+  std::memset(d, 0, sizeof(*d));
+  d->ndim = ndim;
+  for (int k = 0; k < ndim; ++k) {
+    d->sizes[k] = sizes[k];
+    d->strides[k] = strides[k];
+  }
+}
+
+// pack (dst contiguous) or unpack (dst strided); either side may be mapped host memory
+template <bool PACK>
+int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_t* sizes_in,
+                  const int64_t* strides_in, int elem, cudaStream_t s) {
+  int64_t sizes[LMS_MAX_DIMS + 1], strides[LMS_MAX_DIMS + 1];
+  // squeeze size-1 dims; widen 16-byte elements into two 8-byte words
+  int nd = 0;
+  for (int k = 0; k < ndim; ++k) {
+    if (sizes_in[k] == 1) continue;
+    sizes[nd] = sizes_in[k];
+    strides[nd] = strides_in[k];
+    ++nd;
+  }
+  if (elem == 16) {
+    for (int k = 0; k < nd; ++k) strides[k] *= 2;
+    sizes[nd] = 2;
+    strides[nd] = 1;
+    ++nd;
+    elem = 8;
+  }
+  if (nd == 0) {
+    sizes[0] = 1;
+    strides[0] = 1;
+    nd = 1;
+  }
+  if (nd > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "too many dimensions");
+  if (elem != 1 && elem != 2 && elem != 4 && elem != 8) return fail(LMS_E_INVALID, "unsupported element size");
+  int64_t numel = 1;
+  for (int k = 0; k < nd; ++k) numel *= sizes[k];
+  if (numel == 0) return LMS_OK;
+  Strided d;
+  to_desc(&d, nd, sizes, strides);
+#define DISPATCH_E(KERNEL, ...)                                                       \
+  switch (elem) {                                                                     \
+    case 1: KERNEL<PACK, 1><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                  \
+    case 2: KERNEL<PACK, 2><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                  \
+    case 4: KERNEL<PACK, 4><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                  \
+    default: KERNEL<PACK, 8><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                 \
+  }
+  const int last = nd - 1;
+  if (strides[last] == 1) {
+    int64_t row = sizes[last], rows = numel / row;
+    bool vec = (row * elem) % 16 == 0 && (reinterpret_cast<uintptr_t>(dst) % 16 == 0) &&
+               (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    for (int k = 0; k < last && vec; ++k) vec = (strides[k] * elem) % 16 == 0;
+    int grid = sm_grid(c, rows, 8);
+    if (vec) {
+      switch (elem) {
+        case 1: rows_kernel<PACK, true, 1><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+        case 2: rows_kernel<PACK, true, 2><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+        case 4: rows_kernel<PACK, true, 4><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+        default: rows_kernel<PACK, true, 8><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+      }
+    } else {
+      switch (elem) {
+        case 1: rows_kernel<PACK, false, 1><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+        case 2: rows_kernel<PACK, false, 2><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+        case 4: rows_kernel<PACK, false, 4><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+        default: rows_kernel<PACK, false, 8><<<grid, 256, 0, s>>>(dst, src, d, rows, row); break;
+      }
+    }
+  } else {
+    int cd = -1;
+    for (int k = 0; k < last; ++k)
+      if (strides[k] == 1) cd = k;
+    if (cd >= 0 && sizes[cd] >= 8 && sizes[last] >= 8) {
+      int64_t batches = numel / (sizes[cd] * sizes[last]);
+      int64_t tiles = batches * ((sizes[cd] + 31) / 32) * ((sizes[last] + 31) / 32);
+      int grid = sm_grid(c, tiles, 1);
+      DISPATCH_E(transpose_kernel, dst, src, d, cd, batches);
+    } else {
+      int grid = sm_grid(c, numel, 256 * 4);
+      DISPATCH_E(generic_kernel, dst, src, d, numel);
+    }
+  }
+#undef DISPATCH_E
+  c->st.kernel_launches++;
+  CK(cudaGetLastError());
+  return LMS_OK;
+}
+
+int launch_copy(lms_ctx* c, char* dst, const char* src, size_t bytes, cudaStream_t s) {
+  size_t n16 = bytes / 16;
+  if (n16) {
+    int grid = sm_grid(c, int64_t(n16), 512 * 4);
+    copy16_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
+                                       int64_t(n16));
+    c->st.kernel_launches++;
+  }
+  if (bytes % 16) {
+    copy_tail_kernel<<<1, 32, 0, s>>>(dst + n16 * 16, src + n16 * 16, int64_t(bytes % 16));
+    c->st.kernel_launches++;
+  }
+  CK(cudaGetLastError());
+  return LMS_OK;
+}
+
+int ensure_zvc_scratch(lms_ctx* c, size_t words) {
+  if (words <= c->zvc_scratch_words) return LMS_OK;
+  if (c->zvc_scratch) {
+    CK(cudaStreamSynchronize(c->d2h));
+    cudaFree(c->zvc_scratch);
+    c->zvc_scratch = nullptr;
+  }
+  size_t w = std::max(words, size_t(1) << 16);
+  CK(cudaMalloc(&c->zvc_scratch, w * 4));
+  c->zvc_scratch_words = w;
+  return LMS_OK;
+}
+
+int launch_zvc_encode(lms_ctx* c, const uint32_t* src, uint64_t nwords, char* out, cudaStream_t s) {
+  uint64_t ntiles = zvc_tiles(nwords);
+  int rc = ensure_zvc_scratch(c, 2 * (ntiles + 1));
+  if (rc) return rc;
+  uint32_t* counts = c->zvc_scratch;
+  uint32_t* offsets = c->zvc_scratch + ntiles + 1;
+  int grid = sm_grid(c, int64_t(ntiles), 1);
+  zvc_count_kernel<<<grid, 256, 0, s>>>(src, nwords, counts);
+  zvc_scan_kernel<<<1, 1024, 0, s>>>(counts, nwords, offsets, out);
+  zvc_encode_kernel<<<grid, 256, 0, s>>>(src, nwords, offsets, out);
+  c->st.kernel_launches += 3;
+  CK(cudaGetLastError());
+  return LMS_OK;
+}
+
+int launch_zvc_decode(lms_ctx* c, const char* enc, uint64_t nwords, uint32_t* dst, cudaStream_t s) {
+  int grid = sm_grid(c, int64_t(zvc_tiles(nwords)), 1);
+  zvc_decode_kernel<<<grid, 256, 0, s>>>(enc, nwords, dst);
+  c->st.kernel_launches++;
+  CK(cudaGetLastError());
+  return LMS_OK;
+}
+
+void timing_begin(lms_ctx* c, cudaStream_t s, cudaEvent_t* start) {
+  *start = nullptr;
+  if (!c->cfg.timing) return;
+  *start = c->events.get(true);
+  cudaEventRecord(*start, s);
+}
+
+void timing_end(lms_ctx* c, cudaStream_t s, cudaEvent_t start, lms_handle* h, int dir, uint64_t logical,
+                uint64_t wire) {
+  if (!c->cfg.timing || !start) return;
+  cudaEvent_t end = c->events.get(true);
+  cudaEventRecord(end, s);
+  c->recs.push_back({h->id, dir, h->codec, logical, wire, start, end});
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+const char* lms_last_error(void) { return g_err.c_str(); }
+const char* lms_version(void) { return "lms 0.1.0 sm_100a"; }
+
+int lms_default_config(lms_config_t* cfg) {
+  if (!cfg) return fail(LMS_E_INVALID, "null config");
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->host_chunk = size_t(1) << 30;
+  cfg->overlap_transfers = 1;
+  return LMS_OK;
+}
+
+int lms_create(const lms_config_t* cfg, lms_ctx** out) {
+  if (!cfg || !out) return fail(LMS_E_INVALID, "null argument");
+  auto* c = new lms_ctx();
+  c->cfg = *cfg;
+  c->device = cfg->device;
+  c->limit = cfg->device_limit;
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(LMS_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  // transfers get the higher priority so their small kernels are not starved
+  if (cudaStreamCreateWithPriority(&c->d2h, cudaStreamNonBlocking, hi) != cudaSuccess) {
+    delete c;
+    return fail(LMS_E_CUDA, "stream creation failed");
+  }
+  if (cfg->overlap_transfers) {
+    cudaStreamCreateWithPriority(&c->h2d, cudaStreamNonBlocking, hi);
+  } else {
+    c->h2d = c->d2h;
+  }
+  if (cfg->device_reserve) {
+    int rc = ensure_arena(c);
+    if (rc) {
+      delete c;
+      return rc;
+    }
+  }
+  if (cfg->host_reserve) {
+    void* p = nullptr;
+    size_t keep = c->cfg.host_chunk;
+    c->cfg.host_chunk = cfg->host_reserve;
+    int rc = host_alloc_locked(c, 1, &p);
+    c->cfg.host_chunk = keep;
+    if (rc) {
+      delete c;
+      return rc;
+    }
+    host_free_locked(c, p);
+  }
+  c->epoch = c->events.get(true);
+  cudaEventRecord(c->epoch, c->d2h);
+  *out = c;
+  return LMS_OK;
+}
+
+int lms_destroy(lms_ctx* c) {
+  if (!c) return LMS_OK;
+  cudaDeviceSynchronize();
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    reap_zombies(c);
+  }
+  if (g_global == c) g_global = nullptr;
+  for (auto& ch : c->chunks) {
+    cudaFreeHost(ch.base);
+    delete ch.arena;
+  }
+  if (c->dev_base) cudaFree(c->dev_base);
+  if (c->zvc_scratch) cudaFree(c->zvc_scratch);
+  if (c->h2d && c->h2d != c->d2h) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  delete c;
+  return LMS_OK;
+}
+
+int lms_set_global(lms_ctx* c) {
+  g_global = c;
+  return LMS_OK;
+}
+lms_ctx* lms_get_global(void) { return g_global; }
+
+int lms_set_home_stream(lms_ctx* c, void* s) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  c->home = s;
+  return LMS_OK;
+}
+
+int lms_set_limit(lms_ctx* c, size_t limit) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  c->limit = limit;
+  c->cfg.device_limit = limit;
+  if (c->dev_base && (limit == 0 || limit > c->dev.capacity())) c->limit = c->dev.capacity();
+  return LMS_OK;
+}
+
+int lms_reset_peaks(lms_ctx* c) {
+  std::lock_guard<std::mutex> g(c->mu);
+  c->dev.reset_peak();
+  c->host_peak = c->host_used;
+  return LMS_OK;
+}
+
+int lms_get_streams(lms_ctx* c, void** d2h, void** h2d) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  if (d2h) *d2h = c->d2h;
+  if (h2d) *h2d = c->h2d;
+  return LMS_OK;
+}
+
+int lms_dev_alloc(lms_ctx* c, size_t size, void* stream, void** out) {
+  if (!c || !out) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  return dev_alloc_locked(c, size, stream, out);
+}
+
+int lms_dev_free(lms_ctx* c, void* ptr, void* stream) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  return dev_free_locked(c, ptr, stream);
+}
+
+int lms_dev_hold_until(lms_ctx* c, const void* ptr, void* stream) {
+  if (!c || !ptr) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!c->dev.owns(ptr)) return LMS_OK;  // not ours (e.g. default allocator): nothing to hold
+  Block* b = c->dev.containing(static_cast<const char*>(ptr) - c->dev_base);
+  if (!b) return fail(LMS_E_INVALID, "lms_dev_hold_until: pointer not in a live block");
+  auto* ev = new SharedEv();
+  ev->e = c->events.get();
+  ev->refs = 1;
+  CK(cudaEventRecord(ev->e, static_cast<cudaStream_t>(stream)));
+  c->holds[b].push_back(ev);
+  return LMS_OK;
+}
+
+int lms_host_alloc(lms_ctx* c, size_t size, void** out) {
+  if (!c || !out) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  return host_alloc_locked(c, size, out);
+}
+
+int lms_host_free(lms_ctx* c, void* ptr) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  return host_free_locked(c, ptr);
+}
+
+int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_t* strides, int ndim,
+                 int elem_size, void* producer_stream, int codec, lms_handle** out) {
+  if (!c || !out || (ndim > 0 && (!sizes || !strides))) return fail(LMS_E_INVALID, "null argument");
+  if (ndim < 0 || ndim > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "ndim out of range");
+  if (elem_size <= 0) return fail(LMS_E_INVALID, "elem_size must be positive");
+  for (int k = 0; k < ndim; ++k)
+    if (sizes[k] < 0 || strides[k] < 0) return fail(LMS_E_INVALID, "negative size or stride");
+  std::lock_guard<std::mutex> g(c->mu);
+  reap_zombies(c);
+  auto* h = new lms_handle();
+  h->id = c->next_id++;
+  h->ndim = ndim;
+  h->elem = elem_size;
+  for (int k = 0; k < ndim; ++k) {
+    h->sizes[k] = sizes[k];
+    h->strides[k] = strides[k];
+  }
+  bool dense = dense_layout(ndim, sizes, strides, &h->span, &h->numel);
+  h->packed = !dense;
+  h->logical = uint64_t(h->numel) * elem_size;
+  const uint64_t stored = h->packed ? h->logical : uint64_t(h->span) * elem_size;
+  const bool aligned = reinterpret_cast<uintptr_t>(src) % 16 == 0;
+  if (codec == LMS_CODEC_ZVC && (h->packed || stored % 4 != 0 || !aligned)) codec = LMS_CODEC_RAW_SM;
+  if (codec == LMS_CODEC_RAW_SM && !h->packed && !aligned) codec = LMS_CODEC_RAW_CE;
+  if (h->packed) codec = LMS_CODEC_RAW_SM;  // fused pack straight into pinned memory
+  h->codec = codec;
+  h->host_bytes = codec == LMS_CODEC_ZVC ? zvc_bound(stored / 4) : (stored ? stored : 16);
+  int rc = host_alloc_locked(c, h->host_bytes, reinterpret_cast<void**>(&h->host));
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  // the D2H channel starts after the producer's enqueued work
+  cudaStream_t s = c->d2h;
+  stream_wait_on(c, s, producer_stream);
+  c->st.n_cross_stream_waits--;  // the producer dependency is the swap edge, not a pool wait
+  cudaEvent_t t0;
+  timing_begin(c, s, &t0);
+  if (stored) {
+    if (codec == LMS_CODEC_RAW_CE) {
+      CK(cudaMemcpyAsync(h->host, src, stored, cudaMemcpyDeviceToHost, s));
+      h->wire = stored;
+    } else if (codec == LMS_CODEC_RAW_SM) {
+      if (h->packed)
+        rc = launch_layout<true>(c, h->host, static_cast<const char*>(src), ndim, sizes, strides, elem_size, s);
+      else
+        rc = launch_copy(c, h->host, static_cast<const char*>(src), stored, s);
+      h->wire = stored;
+    } else {
+      rc = launch_zvc_encode(c, static_cast<const uint32_t*>(src), stored / 4, h->host, s);
+      h->wire = h->host_bytes;  // upper bound until the header is readable
+    }
+    if (rc) {
+      host_free_locked(c, h->host);
+      delete h;
+      return rc;
+    }
+  }
+  h->out_done = new SharedEv();
+  h->out_done->e = c->events.get();
+  h->out_done->refs = 1;
+  CK(cudaEventRecord(h->out_done->e, s));
+  if (c->cfg.timing && t0) h->rec_out = int64_t(c->recs.size());
+  timing_end(c, s, t0, h, 0, h->logical, h->wire);
+  if (codec == LMS_CODEC_ZVC && stored) {
+    h->wire_known = false;
+    c->zvc_open.push_back(h);
+  }
+  // hold the source block until the copy is done
+  if (stored && c->dev_base && c->dev.owns(src)) {
+    Block* b = c->dev.containing(static_cast<const char*>(src) - c->dev_base);
+    if (b) {
+      h->out_done->refs++;
+      c->holds[b].push_back(h->out_done);
+    }
+  }
+  c->st.n_swap_out++;
+  c->st.n_handles_live++;
+  c->st.d2h_logical_bytes += h->logical;
+  if (codec != LMS_CODEC_ZVC) c->st.d2h_wire_bytes += h->wire;
+  *out = h;
+  return LMS_OK;
+}
+
+int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides, void* trigger_stream) {
+  if (!c || !h) return fail(LMS_E_INVALID, "null argument");
+  if (!dst && h->numel > 0) return fail(LMS_E_INVALID, "null destination");
+  std::lock_guard<std::mutex> g(c->mu);
+  if (h->released) return fail(LMS_E_STATE, "swap_in of a released handle");
+  cudaStream_t s = c->h2d;
+  // gate: the control op (everything enqueued on the trigger stream) and the swap-out
+  stream_wait_on(c, s, trigger_stream);
+  c->st.n_cross_stream_waits--;
+  CK(cudaStreamWaitEvent(s, h->out_done->e, 0));
+  // ZVC: the exact compressed size is known if the swap-out already finished;
+  // otherwise the H2D moves the worst-case bound (correct, just more bytes)
+  account_zvc(c);
+  bool natural = dst_strides == nullptr;
+  if (!natural && !h->packed) {
+    natural = true;
+    for (int k = 0; k < h->ndim; ++k)
+      if (h->sizes[k] > 1 && dst_strides[k] != h->strides[k]) natural = false;
+  }
+  if (!natural && h->packed) {
+    // contiguous strides requested on a packed handle are its natural layout
+    natural = true;
+    int64_t acc = 1;
+    for (int k = h->ndim - 1; k >= 0; --k) {
+      if (h->sizes[k] > 1 && dst_strides[k] != acc) natural = false;
+      acc *= h->sizes[k];
+    }
+  }
+  const uint64_t stored = h->packed ? h->logical : uint64_t(h->span) * h->elem;
+  cudaEvent_t t0;
+  timing_begin(c, s, &t0);
+  uint64_t wire = 0;
+  int rc = LMS_OK;
+  if (stored) {
+    if (!natural) {
+      // arbitrary destination layout: scatter straight out of pinned memory
+      if (h->codec == LMS_CODEC_ZVC) return fail(LMS_E_INVALID, "ZVC handles restore to their own layout");
+      if (!h->packed)
+        return fail(LMS_E_INVALID, "a dense view restores only into its own strides (pass NULL)");
+      rc = launch_layout<false>(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
+      wire = stored;
+    } else if (h->codec == LMS_CODEC_ZVC) {
+      uint64_t bytes = h->wire_known ? h->wire : h->host_bytes;
+      void* stage = nullptr;
+      rc = dev_alloc_locked(c, bytes, s, &stage);
+      if (rc == LMS_OK) {
+        CK(cudaMemcpyAsync(stage, h->host, bytes, cudaMemcpyHostToDevice, s));
+        rc = launch_zvc_decode(c, static_cast<char*>(stage), stored / 4, static_cast<uint32_t*>(dst), s);
+        dev_free_locked(c, stage, s);
+      } else {
+        return rc;  // no room for the staging copy under the budget
+      }
+      wire = bytes;
+    } else if (h->codec == LMS_CODEC_RAW_SM && reinterpret_cast<uintptr_t>(dst) % 16 == 0) {
+      rc = launch_copy(c, static_cast<char*>(dst), h->host, stored, s);
+      wire = stored;
+    } else {
+      CK(cudaMemcpyAsync(dst, h->host, stored, cudaMemcpyHostToDevice, s));
+      wire = stored;
+    }
+  }
+  if (rc) return rc;
+  if (!h->in_ready) h->in_ready = c->events.get();
+  CK(cudaEventRecord(h->in_ready, s));
+  if (c->cfg.timing && t0) h->rec_in = int64_t(c->recs.size());
+  timing_end(c, s, t0, h, 1, h->logical, wire);
+  c->st.n_swap_in++;
+  c->st.h2d_logical_bytes += h->logical;
+  c->st.h2d_wire_bytes += wire;
+  return LMS_OK;
+}
+
+int lms_swap_wait(lms_ctx* c, lms_handle* h, void* consumer_stream) {
+  if (!c || !h) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!h->in_ready) return fail(LMS_E_STATE, "swap_wait before swap_in");
+  if (c->cfg.timing && h->rec_in >= 0) {
+    cudaEvent_t reach = c->events.get(true);
+    CK(cudaEventRecord(reach, static_cast<cudaStream_t>(consumer_stream)));
+    c->waits.push_back({reach, h->rec_in});
+  }
+  CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), h->in_ready, 0));
+  return LMS_OK;
+}
+
+int lms_swap_out_done(lms_ctx* c, lms_handle* h) {
+  if (!c || !h) return fail(LMS_E_INVALID, "null argument");
+  return cudaEventQuery(h->out_done->e) == cudaSuccess ? 1 : 0;
+}
+
+int lms_handle_release(lms_ctx* c, lms_handle* h) {
+  if (!c || !h) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  if (h->released) return fail(LMS_E_STATE, "double release");
+  h->released = true;
+  c->st.n_handles_live--;
+  c->zombie.push_back(h);
+  reap_zombies(c);
+  return LMS_OK;
+}
+
+int lms_handle_info(lms_handle* h, int64_t* id, uint64_t* logical, uint64_t* wire, int* codec) {
+  if (!h) return fail(LMS_E_INVALID, "null handle");
+  if (!h->wire_known && cudaEventQuery(h->out_done->e) == cudaSuccess) {
+    const ZvcHeader* hd = reinterpret_cast<const ZvcHeader*>(h->host);
+    if (hd->magic == kZvcMagic) h->wire = hd->bytes;
+  }
+  if (id) *id = h->id;
+  if (logical) *logical = h->logical;
+  if (wire) *wire = h->wire;
+  if (codec) *codec = h->codec;
+  return LMS_OK;
+}
+
+int lms_handle_layout(lms_handle* h, int64_t* strides_out, int64_t* storage_elems) {
+  if (!h) return fail(LMS_E_INVALID, "null handle");
+  if (h->packed) {
+    int64_t acc = 1;
+    for (int k = h->ndim - 1; k >= 0; --k) {
+      if (strides_out) strides_out[k] = acc;
+      acc *= h->sizes[k];
+    }
+    if (storage_elems) *storage_elems = h->numel;
+  } else {
+    for (int k = 0; k < h->ndim; ++k)
+      if (strides_out) strides_out[k] = h->strides[k];
+    if (storage_elems) *storage_elems = h->span;
+  }
+  return LMS_OK;
+}
+
+int lms_pack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, const int64_t* strides, int ndim,
+             int elem_size, void* stream) {
+  if (!c || !dst || !src) return fail(LMS_E_INVALID, "null argument");
+  if (ndim < 0 || ndim > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "ndim out of range");
+  return launch_layout<true>(c, static_cast<char*>(dst), static_cast<const char*>(src), ndim, sizes, strides,
+                             elem_size, static_cast<cudaStream_t>(stream));
+}
+
+int lms_unpack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, const int64_t* strides, int ndim,
+               int elem_size, void* stream) {
+  if (!c || !dst || !src) return fail(LMS_E_INVALID, "null argument");
+  if (ndim < 0 || ndim > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "ndim out of range");
+  return launch_layout<false>(c, static_cast<char*>(dst), static_cast<const char*>(src), ndim, sizes, strides,
+                              elem_size, static_cast<cudaStream_t>(stream));
+}
+
+size_t lms_zvc_bound(size_t nwords) { return zvc_bound(nwords); }
+
+int lms_zvc_encode(lms_ctx* c, const void* src, size_t nwords, void* dst, void* stream) {
+  if (!c || !src || !dst) return fail(LMS_E_INVALID, "null argument");
+  if (reinterpret_cast<uintptr_t>(src) % 16 || reinterpret_cast<uintptr_t>(dst) % 16)
+    return fail(LMS_E_INVALID, "zvc buffers must be 16-byte aligned");
+  std::lock_guard<std::mutex> g(c->mu);
+  return launch_zvc_encode(c, static_cast<const uint32_t*>(src), nwords, static_cast<char*>(dst),
+                           static_cast<cudaStream_t>(stream));
+}
+
+int lms_zvc_decode(lms_ctx* c, const void* enc, size_t nwords, void* dst, void* stream) {
+  if (!c || !enc || !dst) return fail(LMS_E_INVALID, "null argument");
+  return launch_zvc_decode(c, static_cast<const char*>(enc), nwords, static_cast<uint32_t*>(dst),
+                           static_cast<cudaStream_t>(stream));
+}
+
+int lms_zvc_encoded_size(const void* enc_host, size_t* out) {
+  if (!enc_host || !out) return fail(LMS_E_INVALID, "null argument");
+  const ZvcHeader* h = static_cast<const ZvcHeader*>(enc_host);
+  if (h->magic != kZvcMagic) return fail(LMS_E_INVALID, "not a ZVC stream");
+  *out = h->bytes;
+  return LMS_OK;
+}
+
+int lms_stats(lms_ctx* c, lms_stats_t* out) {
+  if (!c || !out) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  reap_deferred(c, false);
+  account_zvc(c);
+  lms_stats_t s = c->st;
+  s.device_in_use = c->dev.used();
+  s.device_peak = c->dev.peak();
+  s.device_reserved = c->dev.capacity();
+  s.device_limit = c->limit;
+  s.device_largest_free = c->dev.largest_free();
+  s.device_deferred_bytes = c->deferred_bytes;
+  s.host_in_use = c->host_used;
+  s.host_peak = c->host_peak;
+  s.host_reserved = c->host_reserved;
+  double d2h = 0, h2d = 0;
+  for (auto& r : c->recs) {
+    if (cudaEventQuery(r.end) != cudaSuccess) continue;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.start, r.end);
+    (r.direction == 0 ? d2h : h2d) += ms;
+  }
+  s.d2h_busy_ms = d2h;
+  s.h2d_busy_ms = h2d;
+  double stall = 0;
+  for (auto& w : c->waits) {
+    const XferRec& r = c->recs[w.second];
+    if (cudaEventQuery(w.first) != cudaSuccess || cudaEventQuery(r.end) != cudaSuccess) continue;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, w.first, r.end);
+    if (ms > 0) stall += ms;
+  }
+  s.swap_wait_ms = stall;
+  *out = s;
+  return LMS_OK;
+}
+
+int lms_trace(lms_ctx* c, lms_xfer_record_t* out, size_t cap, size_t* n) {
+  if (!c || !n) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  size_t k = 0;
+  for (auto& r : c->recs) {
+    if (k >= cap) break;
+    if (cudaEventQuery(r.end) != cudaSuccess) continue;
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, c->epoch, r.start);
+    cudaEventElapsedTime(&b, c->epoch, r.end);
+    if (out) out[k] = {r.handle_id, r.direction, r.codec, r.logical, r.wire, a, b};
+    ++k;
+  }
+  *n = k;
+  return LMS_OK;
+}
+
+int lms_trace_clear(lms_ctx* c) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  cudaStreamSynchronize(c->d2h);
+  cudaStreamSynchronize(c->h2d);
+  for (auto& r : c->recs) {
+    c->events.put(r.start, true);
+    c->events.put(r.end, true);
+  }
+  c->recs.clear();
+  for (auto& w : c->waits) c->events.put(w.first, true);
+  c->waits.clear();
+  cudaEventRecord(c->epoch, c->d2h);
+  c->st.d2h_logical_bytes = c->st.d2h_wire_bytes = 0;
+  c->st.h2d_logical_bytes = c->st.h2d_wire_bytes = 0;
+  c->st.n_swap_out = c->st.n_swap_in = 0;
+  c->st.kernel_launches = 0;
+  return LMS_OK;
+}
+
+int lms_synchronize(lms_ctx* c) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  CK(cudaStreamSynchronize(c->d2h));
+  CK(cudaStreamSynchronize(c->h2d));
+  std::lock_guard<std::mutex> g(c->mu);
+  reap_deferred(c, false);
+  reap_zombies(c);
+  return LMS_OK;
+}
+
+// PyTorch CUDAPluggableAllocator hooks.  The pluggable ABI has no error
+// channel, so an exhausted budget is reported by throwing: PyTorch's Python
+// boundary turns it into a RuntimeError whose text starts with "LMS_OOM".
+void* lms_alloc(size_t size, int device, void* stream) {
+  lms_ctx* c = g_global;
+  if (!c) throw std::runtime_error("LMS: allocator hook called before lms_set_global");
+  (void)device;
+  void* p = nullptr;
+  int rc;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    rc = dev_alloc_locked(c, size, stream, &p);
+  }
+  if (rc != LMS_OK) throw OomError(g_err);
+  return p;
+}
+
+void lms_free(void* ptr, size_t size, int device, void* stream) {
+  (void)size;
+  (void)device;
+  lms_ctx* c = g_global;
+  if (!c) return;
+  std::lock_guard<std::mutex> g(c->mu);
+  dev_free_locked(c, ptr, stream);
+}
+
+}  // extern "C"

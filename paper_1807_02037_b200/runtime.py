@@ -1,0 +1,318 @@
+"""Python binding of liblms.so (ctypes over the C ABI in include/lms.h).
+
+This is plumbing: it turns torch tensors and streams into the plain pointers
+and handles the C layer takes, and turns negative return codes into the
+exception types the reference uses (``ValueError`` family for bad input,
+``RuntimeError`` for runtime failures).  There is no fallback: if the
+library is missing or CUDA is unavailable, using a :class:`Context` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblms.so")
+
+LMS_OK, LMS_E_INVALID, LMS_E_OOM, LMS_E_HOST_OOM, LMS_E_CUDA, LMS_E_STATE = 0, -1, -2, -3, -4, -5
+CODEC_RAW_CE, CODEC_RAW_SM, CODEC_ZVC = 0, 1, 2
+CODECS = {"ce": CODEC_RAW_CE, "sm": CODEC_RAW_SM, "zvc": CODEC_ZVC}
+MAX_DIMS = 8
+
+
+class LmsError(RuntimeError):
+    """A liblms call failed."""
+
+
+class LmsOutOfMemoryError(LmsError):
+    """The enforced device budget cannot satisfy an allocation (SimReport.oom analogue)."""
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("device_reserve", ctypes.c_size_t),
+                ("device_limit", ctypes.c_size_t), ("host_reserve", ctypes.c_size_t),
+                ("host_chunk", ctypes.c_size_t), ("overlap_transfers", ctypes.c_int),
+                ("timing", ctypes.c_int), ("sm_ctas", ctypes.c_int)]
+
+
+_STAT_FIELDS = [
+    "device_in_use", "device_peak", "device_reserved", "device_limit", "device_largest_free",
+    "device_deferred_bytes", "host_in_use", "host_peak", "host_reserved", "n_alloc", "n_free",
+    "n_oom", "n_deferred_frees", "n_cross_stream_waits", "n_swap_out", "n_swap_in",
+    "n_handles_live", "d2h_logical_bytes", "d2h_wire_bytes", "h2d_logical_bytes",
+    "h2d_wire_bytes", "kernel_launches",
+]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint64) for f in _STAT_FIELDS] + [
+        ("d2h_busy_ms", ctypes.c_double), ("h2d_busy_ms", ctypes.c_double),
+        ("swap_wait_ms", ctypes.c_double)]
+
+
+class _Xfer(ctypes.Structure):
+    _fields_ = [("handle_id", ctypes.c_int64), ("direction", ctypes.c_int), ("codec", ctypes.c_int),
+                ("logical_bytes", ctypes.c_uint64), ("wire_bytes", ctypes.c_uint64),
+                ("start_ms", ctypes.c_double), ("end_ms", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load liblms.so once; raise if it was not built (no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise LmsError(f"{LIB_PATH} is missing; run __graft_entry__.build() "
+                       f"(make -C paper_1807_02037_b200/csrc)")
+    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    vp, sz, i, i64p = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)
+    pp = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "lms_last_error": ([], ctypes.c_char_p), "lms_version": ([], ctypes.c_char_p),
+        "lms_default_config": ([ctypes.POINTER(_Config)], i),
+        "lms_create": ([ctypes.POINTER(_Config), pp], i), "lms_destroy": ([vp], i),
+        "lms_set_global": ([vp], i), "lms_get_global": ([], vp),
+        "lms_set_home_stream": ([vp, vp], i), "lms_set_limit": ([vp, sz], i),
+        "lms_reset_peaks": ([vp], i), "lms_get_streams": ([vp, pp, pp], i),
+        "lms_dev_alloc": ([vp, sz, vp, pp], i), "lms_dev_free": ([vp, vp, vp], i),
+        "lms_dev_hold_until": ([vp, vp, vp], i),
+        "lms_host_alloc": ([vp, sz, pp], i), "lms_host_free": ([vp, vp], i),
+        "lms_swap_out": ([vp, vp, i64p, i64p, i, i, vp, i, pp], i),
+        "lms_swap_in": ([vp, vp, vp, i64p, vp], i), "lms_swap_wait": ([vp, vp, vp], i),
+        "lms_swap_out_done": ([vp, vp], i), "lms_handle_release": ([vp, vp], i),
+        "lms_handle_info": ([vp, i64p, ctypes.POINTER(ctypes.c_uint64),
+                             ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(i)], i),
+        "lms_handle_layout": ([vp, i64p, i64p], i),
+        "lms_pack": ([vp, vp, vp, i64p, i64p, i, i, vp], i),
+        "lms_unpack": ([vp, vp, vp, i64p, i64p, i, i, vp], i),
+        "lms_zvc_bound": ([sz], sz), "lms_zvc_encode": ([vp, vp, sz, vp, vp], i),
+        "lms_zvc_decode": ([vp, vp, sz, vp, vp], i),
+        "lms_zvc_encoded_size": ([vp, ctypes.POINTER(sz)], i),
+        "lms_stats": ([vp, ctypes.POINTER(_Stats)], i),
+        "lms_trace": ([vp, ctypes.POINTER(_Xfer), sz, ctypes.POINTER(sz)], i),
+        "lms_trace_clear": ([vp], i), "lms_synchronize": ([vp], i),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def _check(rc: int, what: str):
+    if rc == LMS_OK:
+        return
+    msg = f"{what}: {lib().lms_last_error().decode()}"
+    if rc == LMS_E_INVALID:
+        raise ValueError(msg)
+    if rc == LMS_E_OOM:
+        raise LmsOutOfMemoryError(msg)
+    raise LmsError(msg)
+
+
+def _i64(vals):
+    arr = (ctypes.c_int64 * max(1, len(vals)))(*vals)
+    return arr
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+@dataclass
+class SwapHandle:
+    """Host copy of one swapped tensor (opaque ``lms_handle*``)."""
+
+    ptr: int
+    id: int
+    shape: tuple
+    dtype: object
+    logical_bytes: int
+    restore_strides: tuple
+    storage_elems: int
+    released: bool = False
+
+
+class Context:
+    """One device's pools and swap channels (``lms_ctx``)."""
+
+    def __init__(self, device: int = 0, device_reserve: int = 0, device_limit: int = 0,
+                 host_reserve: int = 0, host_chunk: int = 1 << 30, overlap_transfers: bool = True,
+                 timing: bool = False, sm_ctas: int = 0):
+        L = lib()
+        cfg = _Config()
+        _check(L.lms_default_config(ctypes.byref(cfg)), "lms_default_config")
+        cfg.device, cfg.device_reserve, cfg.device_limit = device, device_reserve, device_limit
+        cfg.host_reserve, cfg.host_chunk = host_reserve, host_chunk
+        cfg.overlap_transfers, cfg.timing, cfg.sm_ctas = int(overlap_transfers), int(timing), sm_ctas
+        out = ctypes.c_void_p()
+        _check(L.lms_create(ctypes.byref(cfg), ctypes.byref(out)), "lms_create")
+        self.ptr = out.value
+        self.device = device
+        self.timing = timing
+
+    # -- lifetime -------------------------------------------------------------
+    def close(self):
+        if self.ptr:
+            _check(lib().lms_destroy(self.ptr), "lms_destroy")
+            self.ptr = None
+
+    def make_global(self):
+        _check(lib().lms_set_global(self.ptr), "lms_set_global")
+
+    def set_limit(self, nbytes: int):
+        _check(lib().lms_set_limit(self.ptr, nbytes), "lms_set_limit")
+
+    def reset_peaks(self):
+        _check(lib().lms_reset_peaks(self.ptr), "lms_reset_peaks")
+
+    def streams(self):
+        """(d2h, h2d) as torch.cuda.ExternalStream objects."""
+        import torch
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().lms_get_streams(self.ptr, ctypes.byref(a), ctypes.byref(b)), "lms_get_streams")
+        dev = torch.device("cuda", self.device)
+        return (torch.cuda.ExternalStream(a.value, device=dev),
+                torch.cuda.ExternalStream(b.value, device=dev))
+
+    def synchronize(self):
+        _check(lib().lms_synchronize(self.ptr), "lms_synchronize")
+
+    # -- swap engine ------------------------------------------------------------
+    def swap_out(self, t, codec: str | int = "ce", stream=None) -> SwapHandle:
+        """Start moving ``t`` to pinned memory after the work enqueued on ``stream``."""
+        code = CODECS[codec] if isinstance(codec, str) else int(codec)
+        if not t.is_cuda:
+            raise ValueError("swap_out needs a CUDA tensor")
+        if t.dim() > MAX_DIMS:
+            raise ValueError(f"swap_out supports up to {MAX_DIMS} dims")
+        sizes, strides = list(t.shape), list(t.stride())
+        h = ctypes.c_void_p()
+        _check(lib().lms_swap_out(self.ptr, t.data_ptr(), _i64(sizes), _i64(strides), t.dim(),
+                                  t.element_size(), _stream_ptr(stream), code, ctypes.byref(h)),
+               "lms_swap_out")
+        hid = ctypes.c_int64()
+        logical = ctypes.c_uint64()
+        _check(lib().lms_handle_info(h.value, ctypes.byref(hid), ctypes.byref(logical), None, None),
+               "lms_handle_info")
+        rs = (ctypes.c_int64 * max(1, t.dim()))()
+        se = ctypes.c_int64()
+        _check(lib().lms_handle_layout(h.value, rs, ctypes.byref(se)), "lms_handle_layout")
+        return SwapHandle(h.value, hid.value, tuple(sizes), t.dtype, logical.value,
+                          tuple(rs[k] for k in range(t.dim())), se.value)
+
+    def alloc_for(self, h: SwapHandle):
+        """Allocate the swap-in destination in the handle's restore layout."""
+        import torch
+        return torch.empty_strided(h.shape, h.restore_strides, dtype=h.dtype,
+                                   device=torch.device("cuda", self.device))
+
+    def swap_in(self, h: SwapHandle, dst=None, trigger_stream=None):
+        """Start the H2D once the work enqueued on ``trigger_stream`` (the control
+        op) is done.  Returns the destination tensor; call :meth:`wait` before use."""
+        if h.released:
+            raise RuntimeError("swap_in of a released handle")
+        if dst is None:
+            dst = self.alloc_for(h)
+        strides = None if tuple(dst.stride()) == h.restore_strides else _i64(list(dst.stride()))
+        _check(lib().lms_swap_in(self.ptr, h.ptr, dst.data_ptr(), strides, _stream_ptr(trigger_stream)),
+               "lms_swap_in")
+        return dst
+
+    def wait(self, h: SwapHandle, stream=None):
+        _check(lib().lms_swap_wait(self.ptr, h.ptr, _stream_ptr(stream)), "lms_swap_wait")
+
+    def swap_out_done(self, h: SwapHandle) -> bool:
+        return lib().lms_swap_out_done(self.ptr, h.ptr) == 1
+
+    def release(self, h: SwapHandle):
+        if not h.released:
+            h.released = True
+            _check(lib().lms_handle_release(self.ptr, h.ptr), "lms_handle_release")
+
+    def wire_bytes(self, h: SwapHandle) -> int:
+        w = ctypes.c_uint64()
+        _check(lib().lms_handle_info(h.ptr, None, None, ctypes.byref(w), None), "lms_handle_info")
+        return w.value
+
+    # -- pools --------------------------------------------------------------------
+    def hold_until(self, t, stream=None):
+        _check(lib().lms_dev_hold_until(self.ptr, t.data_ptr(), _stream_ptr(stream)), "lms_dev_hold_until")
+
+    # -- staging kernels ----------------------------------------------------------
+    def pack(self, src, out=None, stream=None):
+        """Contiguous copy of a strided view through the sm_100a pack kernels."""
+        import torch
+        if out is None:
+            out = torch.empty(src.shape, dtype=src.dtype, device=src.device)
+        _check(lib().lms_pack(self.ptr, out.data_ptr(), src.data_ptr(), _i64(list(src.shape)),
+                              _i64(list(src.stride())), src.dim(), src.element_size(), _stream_ptr(stream)),
+               "lms_pack")
+        return out
+
+    def unpack(self, src, dst, stream=None):
+        """Scatter contiguous ``src`` into the strided view ``dst``."""
+        _check(lib().lms_unpack(self.ptr, dst.data_ptr(), src.data_ptr(), _i64(list(dst.shape)),
+                                _i64(list(dst.stride())), dst.dim(), dst.element_size(), _stream_ptr(stream)),
+               "lms_unpack")
+        return dst
+
+    def zvc_bound(self, nwords: int) -> int:
+        return lib().lms_zvc_bound(nwords)
+
+    def zvc_encode(self, src, dst, stream=None):
+        _check(lib().lms_zvc_encode(self.ptr, src.data_ptr(), src.numel() * src.element_size() // 4,
+                                    dst.data_ptr(), _stream_ptr(stream)), "lms_zvc_encode")
+
+    def zvc_decode(self, enc, dst, stream=None):
+        _check(lib().lms_zvc_decode(self.ptr, enc.data_ptr(), dst.numel() * dst.element_size() // 4,
+                                    dst.data_ptr(), _stream_ptr(stream)), "lms_zvc_decode")
+
+    # -- reporting ----------------------------------------------------------------
+    def stats(self) -> dict:
+        s = _Stats()
+        _check(lib().lms_stats(self.ptr, ctypes.byref(s)), "lms_stats")
+        return {f: getattr(s, f) for f, _ in _Stats._fields_}
+
+    def trace(self, cap: int = 1 << 16) -> list[dict]:
+        buf = (_Xfer * cap)()
+        n = ctypes.c_size_t()
+        _check(lib().lms_trace(self.ptr, buf, cap, ctypes.byref(n)), "lms_trace")
+        return [{f: getattr(buf[k], f) for f, _ in _Xfer._fields_} for k in range(n.value)]
+
+    def trace_clear(self):
+        _check(lib().lms_trace_clear(self.ptr), "lms_trace_clear")
+
+
+_installed: Context | None = None
+
+
+def install_allocator(ctx: Context):
+    """Route every PyTorch CUDA allocation of this process through ``ctx``'s pool.
+
+    Must run before the first CUDA allocation (PyTorch's rule for
+    ``change_current_allocator``).  Idempotent for the same context.
+    """
+    global _installed
+    import torch
+    if _installed is ctx:
+        return
+    if _installed is not None:
+        raise RuntimeError("a different LMS context already owns the PyTorch allocator")
+    ctx.make_global()
+    alloc = torch.cuda.memory.CUDAPluggableAllocator(LIB_PATH, "lms_alloc", "lms_free")
+    torch.cuda.memory.change_current_allocator(alloc)
+    _installed = ctx
+
+
+def installed_context() -> Context | None:
+    return _installed

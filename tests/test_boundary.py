@@ -1,0 +1,57 @@
+"""The C-ABI boundary: liblms.so loads and exports every symbol include/lms.h declares.
+
+Runs without a GPU (no compute calls).  Also checks the Python facade keeps
+the reference package's import surface (swapgraph/__init__.py:60-115).
+"""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_1807_02037_b200", "liblms.so")
+HEADER = os.path.join(ROOT, "include", "lms.h")
+
+REFERENCE_ALL = [
+    "HOST", "CompGraph", "CtrlQuery", "CycleError", "DeadlockError", "EdgeAction", "EdgeRec",
+    "GraphFormatError", "NodeKind", "OpNode", "Phase", "RewriteConfig", "RewriteError",
+    "RewriteReport", "SimConfig", "SimReport", "TOPOLOGIES", "TensorSpec", "TraceEvent",
+    "Violation", "accelerator", "ancestors", "attach_control", "branchy", "chain", "chain_rule",
+    "compute_node", "constant_node", "direct_order", "dumps", "fallback_control",
+    "fuse_swap_ins", "fuse_swap_outs", "graph_from_dict", "graph_to_dict", "insert_swap_pair",
+    "lifetime", "load_graph", "loads", "reachable", "resnet_like", "resolve_phases", "rewrite",
+    "save_graph", "select_candidates", "to_dot", "topo_order", "unet", "validate",
+    "variable_node", "write_trace_csv",
+]
+
+
+def _declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(lms_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(LIB):
+        pytest.fail("liblms.so not built: run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB)
+    names = _declared()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert missing == []
+    lib.lms_version.restype = ctypes.c_char_p
+    assert b"sm_100a" in lib.lms_version()
+
+
+def test_cubin_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_facade_surface():
+    import paper_1807_02037_b200 as P
+    for name in REFERENCE_ALL:
+        assert hasattr(P, name), name

@@ -1,0 +1,106 @@
+"""Swap engine round trips, budget enforcement and free-after-transfer semantics.
+
+Reference behaviour being realised: swap nodes are identities on values
+(interp.py:168-170); a swapped-out block is freed only after its outbound
+transfer completes (sim.py:205-211); exceeding device capacity is an OOM
+(sim.py:471).
+"""
+
+import pytest
+import torch
+
+from paper_1807_02037_b200 import runtime as rt
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    yield "contig_f32", torch.randn(1024, 1031, device="cuda", generator=g)
+    yield "relu_sparse", torch.relu(torch.randn(64, 256, 56, 56, device="cuda", generator=g))
+    yield "channels_last", torch.randn(8, 64, 28, 28, device="cuda", generator=g).contiguous(
+        memory_format=torch.channels_last)
+    yield "strided_slice", torch.randn(300, 500, device="cuda", generator=g)[:, 100:400]
+    yield "transposed_slice", torch.randn(300, 500, device="cuda", generator=g).t()[10:300]
+    yield "expand", torch.randn(1, 512, device="cuda", generator=g).expand(64, 512)
+    yield "bf16", torch.randn(333, 777, device="cuda", generator=g).bfloat16()
+    yield "odd_bytes", torch.randint(0, 255, (1001,), device="cuda", dtype=torch.uint8)
+    yield "empty", torch.empty(0, 16, device="cuda")
+
+
+@pytest.mark.parametrize("codec", ["ce", "sm", "zvc"])
+def test_roundtrip_bit_exact(lms_ctx, codec):
+    for name, t in _cases():
+        want = t.clone()
+        h = lms_ctx.swap_out(t, codec)
+        out = lms_ctx.swap_in(h)
+        lms_ctx.wait(h)
+        lms_ctx.release(h)
+        torch.cuda.synchronize()
+        assert out.shape == want.shape, name
+        assert torch.equal(out, want), (name, codec)
+
+
+def test_zvc_shrinks_sparse_and_not_dense(lms_ctx):
+    sparse = torch.relu(torch.randn(1 << 22, device="cuda"))
+    dense = torch.randn(1 << 22, device="cuda")
+    hs = lms_ctx.swap_out(sparse, "zvc")
+    hd = lms_ctx.swap_out(dense, "zvc")
+    torch.cuda.synchronize()
+    lms_ctx.synchronize()
+    assert lms_ctx.wire_bytes(hs) < 0.6 * sparse.numel() * 4
+    assert lms_ctx.wire_bytes(hd) <= dense.numel() * 4 + 64  # raw fallback, never bigger
+    for h in (hs, hd):
+        out = lms_ctx.swap_in(h)
+        lms_ctx.wait(h)
+        lms_ctx.release(h)
+    torch.cuda.synchronize()
+
+
+def test_free_waits_for_swap_out(lms_ctx):
+    """Freeing a tensor right after swap_out must not let the block be recycled
+    before the D2H has read it."""
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        t = torch.randn(64 << 20, device="cuda")  # 256 MiB: the copy takes milliseconds
+        want = t[:1024].clone(), t[-1024:].clone()
+        h = lms_ctx.swap_out(t, "ce")
+        del t                                       # free immediately (stream-ordered)
+        junk = torch.full((64 << 20,), 3.0, device="cuda")  # would reuse the block if not held
+        out = lms_ctx.swap_in(h, trigger_stream=s)
+        lms_ctx.wait(h)
+        torch.cuda.synchronize()
+        assert torch.equal(out[:1024], want[0]) and torch.equal(out[-1024:], want[1])
+        lms_ctx.release(h)
+        del junk, out
+
+
+def test_budget_is_enforced(lms_ctx):
+    st = lms_ctx.stats()
+    lms_ctx.set_limit(st["device_in_use"] + (64 << 20))
+    try:
+        a = torch.empty(32 << 20, dtype=torch.uint8, device="cuda")
+        with pytest.raises(RuntimeError, match="LMS_OOM"):
+            torch.empty(128 << 20, dtype=torch.uint8, device="cuda")
+        del a
+    finally:
+        lms_ctx.set_limit(0)
+    assert lms_ctx.stats()["n_oom"] >= 1
+
+
+def test_stats_count_bytes_and_kernels(lms_ctx):
+    lms_ctx.trace_clear()
+    t = torch.relu(torch.randn(1 << 20, device="cuda"))
+    h = lms_ctx.swap_out(t, "zvc")
+    out = lms_ctx.swap_in(h)
+    lms_ctx.wait(h)
+    lms_ctx.release(h)
+    torch.cuda.synchronize()
+    lms_ctx.synchronize()
+    st = lms_ctx.stats()
+    assert st["d2h_logical_bytes"] == 4 << 20 and st["h2d_logical_bytes"] == 4 << 20
+    assert st["kernel_launches"] >= 4  # count, scan, encode, decode
+    assert 0 < st["d2h_wire_bytes"] < 4 << 20
+    tr = lms_ctx.trace()
+    assert {r["direction"] for r in tr} == {0, 1}
+    assert all(r["end_ms"] >= r["start_ms"] for r in tr)
