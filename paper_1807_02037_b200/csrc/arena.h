@@ -119,14 +119,25 @@ class Arena {
     free_.insert({b->size, b});
   }
 
-  // Re-tag a free block (and merge with like-tagged neighbours).
-  void retag_free(Block* b, void* tag) {
-    free_.erase({b->size, b});
-    used_ += b->size;
-    live_[b->off] = b;
-    b->free = false;
-    b->tag = tag;
-    release(b);
+  // Give every free block `tag` and coalesce runs of adjacent free blocks
+  // (used once nothing is pending on any stream, e.g. after a device sync).
+  void retag_all_free(void* tag) {
+    free_.clear();
+    Block* b = head_;
+    while (b) {
+      if (b->free) {
+        b->tag = tag;
+        while (b->next && b->next->free) {
+          Block* n = b->next;
+          b->size += n->size;
+          b->next = n->next;
+          if (n->next) n->next->prev = b;
+          delete n;
+        }
+        free_.insert({b->size, b});
+      }
+      b = b->next;
+    }
   }
 
   bool mergeable(const Block* a, const Block* b) const {

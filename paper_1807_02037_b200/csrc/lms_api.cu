@@ -263,11 +263,7 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
       // merge blocks split by stream tags: after a device sync nothing is pending
       cudaDeviceSynchronize();
       reap_deferred(c, true);
-      std::vector<Block*> fr;
-      c->dev.for_each_free([&](Block* b) { if (b->tag != kFresh) fr.push_back(b); });
-      for (Block* b : fr) {
-        if (b->free) c->dev.retag_free(b, kFresh);
-      }
+      c->dev.retag_all_free(kFresh);
     }
   }
   c->st.n_oom++;
@@ -932,8 +928,15 @@ int lms_handle_layout(lms_handle* h, int64_t* strides_out, int64_t* storage_elem
   return LMS_OK;
 }
 
+static bool view_empty(int ndim, const int64_t* sizes) {
+  for (int k = 0; k < ndim; ++k)
+    if (sizes[k] == 0) return true;
+  return false;
+}
+
 int lms_pack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, const int64_t* strides, int ndim,
              int elem_size, void* stream) {
+  if (c && ndim >= 0 && ndim <= LMS_MAX_DIMS && view_empty(ndim, sizes)) return LMS_OK;
   if (!c || !dst || !src) return fail(LMS_E_INVALID, "null argument");
   if (ndim < 0 || ndim > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "ndim out of range");
   return launch_layout<true>(c, static_cast<char*>(dst), static_cast<const char*>(src), ndim, sizes, strides,
@@ -942,6 +945,7 @@ int lms_pack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, const
 
 int lms_unpack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, const int64_t* strides, int ndim,
                int elem_size, void* stream) {
+  if (c && ndim >= 0 && ndim <= LMS_MAX_DIMS && view_empty(ndim, sizes)) return LMS_OK;
   if (!c || !dst || !src) return fail(LMS_E_INVALID, "null argument");
   if (ndim < 0 || ndim > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "ndim out of range");
   return launch_layout<false>(c, static_cast<char*>(dst), static_cast<const char*>(src), ndim, sizes, strides,

@@ -184,6 +184,7 @@ def execute(g: CompGraph, inputs: dict, cfg: ExecConfig = ExecConfig(), ctx: rt.
     handles: dict[int, rt.SwapHandle] = {}   # swap_out output tensor -> host copy
     handle_uses: dict[int, int] = {}
     tensor_of_handle: dict[int, int] = {}
+    waits_left: dict[int, int] = {}            # id(handle) -> swap-ins not yet waited on
 
     def take(e):
         prod = g.tensor_by_id[e.tensor].producer
@@ -194,6 +195,10 @@ def execute(g: CompGraph, inputs: dict, cfg: ExecConfig = ExecConfig(), ctx: rt.
             if not v.waited:
                 ctx.wait(v.handle, stream)
                 v.waited = True
+                key = id(v.handle)
+                waits_left[key] -= 1
+                if waits_left[key] == 0:
+                    ctx.release(v.handle)  # last swap-in landed for this consumer side
             return v.tensor
         return v
 
@@ -221,6 +226,7 @@ def execute(g: CompGraph, inputs: dict, cfg: ExecConfig = ExecConfig(), ctx: rt.
             for t in produced:
                 handles[t.id] = h
                 handle_uses[t.id] = readers.get(t.id, 0)
+                waits_left[id(h)] = readers.get(t.id, 0)
                 tensor_of_handle[h.id] = _origin(g, t.id, memo)
             continue
         if node.kind is NodeKind.SWAP_IN:
@@ -231,8 +237,6 @@ def execute(g: CompGraph, inputs: dict, cfg: ExecConfig = ExecConfig(), ctx: rt.
             dst = ctx.swap_in(h, trigger_stream=stream)  # control op is already enqueued
             handle_uses[src_t] -= 1
             readers[src_t] -= 1
-            if handle_uses[src_t] == 0:
-                ctx.release(h)  # host copy freed once this H2D has read it
             for t in produced:
                 values[t.id] = _Swapped(dst, h)
             continue

@@ -229,6 +229,8 @@ class Context:
         return dst
 
     def wait(self, h: SwapHandle, stream=None):
+        if h.released:
+            raise RuntimeError("wait on a released handle")
         _check(lib().lms_swap_wait(self.ptr, h.ptr, _stream_ptr(stream)), "lms_swap_wait")
 
     def swap_out_done(self, h: SwapHandle) -> bool:

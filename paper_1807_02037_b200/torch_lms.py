@@ -1,0 +1,534 @@
+"""PyTorch training steps under TFLMS swapping.
+
+This is the caller side of the rewrite: it captures a
+training step as a :class:`~.graph.CompGraph`, runs the unchanged
+:func:`~.rewriter.rewrite` on it, and executes the rewritten schedule with
+liblms:
+
+capture   one traced step records every tensor autograd saves for backward
+          (``saved_tensors_hooks`` pack calls, in order) and, in backward,
+          which autograd node consumed it (``torch._C._current_autograd_node``).
+          The graph has a forward op F(n) and a backward op B(n) per autograd
+          node n (creation order = ``_sequence_nr``), a variable per parameter
+          and per step input, and one update op per parameter.  Saved tensors
+          become F(producer) -> B(consumer) read edges — the paper's
+          forward->backward candidates (PAPER §4.1, rewriter.py:214-238).
+rewrite   the reference algorithm, any ``RewriteConfig`` (n_tensors, lb/ub,
+          chain_rule/direct_order, fuse_swapins, incl/excl types ...).
+execute   pack hook = swap-out: the first pack of a selected tensor starts a
+          D2H on liblms's copy channel (fused swap-outs: one per tensor,
+          rewriter.py:294-334) and autograd keeps only a handle, so the
+          device block returns to the budgeted pool once the D2H is done.
+          Each swap-in group (one rewritten swap-in node; fused groups feed
+          several consumers) is issued by a post-hook on its control op's
+          autograd node, so the H2D starts when that op finishes; the unpack
+          hook only makes the consumer's stream wait on the group's event.
+
+Conventions kept from the reference: swap-ins with no control op are issued
+eagerly right after their swap-out (rewriter.py:472-475); control ops that
+fall in the forward phase fire at the start of backward (an autograd node
+cannot be hooked on its forward execution).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from .graph import (
+    CompGraph,
+    EdgeAction,
+    EdgeRec,
+    NodeKind,
+    OpNode,
+    Phase,
+    TensorSpec,
+    compute_node,
+    variable_node,
+)
+from .rewriter import RewriteConfig, RewriteReport, rewrite
+from . import runtime as rt
+
+_current_node = torch._C._current_autograd_node
+
+
+def _fwd_name(node) -> str:
+    n = node.name()
+    for suffix in ("Backward0", "Backward1", "Backward"):
+        if n.endswith(suffix):
+            return n[: -len(suffix)]
+    return n
+
+
+def _walk(root):
+    """Every autograd node reachable from ``root`` (BFS over next_functions)."""
+    seen = {}
+    todo = [root]
+    while todo:
+        n = todo.pop()
+        if n is None or n in seen:
+            continue
+        seen[n] = True
+        for nxt, _ in n.next_functions:
+            if nxt is not None and nxt not in seen:
+                todo.append(nxt)
+    return list(seen)
+
+
+def _is_accumulate(node) -> bool:
+    return node.name() == "torch::autograd::AccumulateGrad"
+
+
+@dataclass
+class _Saved:
+    """One distinct saved tensor seen at capture."""
+
+    tid: int
+    nbytes: int
+    producer: object            # autograd node, "self" (saved by its own op) or None (leaf)
+    is_param: bool
+    packs: list = field(default_factory=list)   # pack indices that saved it
+
+
+@dataclass
+class SwapGroup:
+    """One swap-in node of the rewritten graph."""
+
+    gid: int
+    saved: int                  # index into plan.saved
+    packs: list                 # pack indices this group serves
+    trigger: int | None         # node rank of the control op's backward node; None = eager
+    trigger_kind: str           # "backward" | "forward->bwd-start" | "eager"
+
+
+@dataclass
+class SwapPlan:
+    """Everything the executor needs, keyed by pack index and node rank."""
+
+    graph: CompGraph
+    rewritten: CompGraph
+    report: RewriteReport
+    n_packs: int
+    pack_saved: list            # pack idx -> saved index (or -1 if kept)
+    saved: list                 # list[_SavedInfo]
+    groups: list                # list[SwapGroup]
+    pack_group: dict            # pack idx -> group id
+    triggers: dict              # node rank -> [group ids]
+    bwd_start_groups: list
+    eager_groups: list
+    swapped_bytes_per_step: int
+    saved_bytes_per_step: int
+    capture_batch: int
+    rewrite_seconds: float
+
+    def summary(self) -> dict:
+        return {
+            "tensors_saved": len(self.saved),
+            "tensors_swapped": self.report.tensors_swapped,
+            "swap_ins": len(self.groups),
+            "control_edges": self.report.control_edges_added,
+            "eager_swap_ins": len(self.eager_groups),
+            "bwd_start_swap_ins": len(self.bwd_start_groups),
+            "swapped_bytes_capture": self.swapped_bytes_per_step,
+            "saved_bytes_capture": self.saved_bytes_per_step,
+            "graph_nodes": len(self.graph.nodes),
+            "rewrite_seconds": self.rewrite_seconds,
+        }
+
+
+@dataclass
+class _SavedInfo:
+    tid: int
+    nbytes: int
+    swapped: bool
+
+
+class _Capture:
+    """Records packs (forward) and consumers (backward) for one traced step."""
+
+    def __init__(self):
+        self.packs = []        # pack idx -> (tensor key, nbytes, grad_fn or None, is_leaf, requires_grad)
+        self.keep = []         # strong refs so addresses stay unique during capture
+        self.consumer = {}     # pack idx -> autograd node that unpacked it
+
+    def pack(self, t):
+        k = len(self.packs)
+        key = (t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype)
+        self.packs.append((key, t.numel() * t.element_size(), t.grad_fn, t.is_leaf,
+                           t.requires_grad, isinstance(t, torch.nn.Parameter)))
+        self.keep.append(t)
+        return (k, t)
+
+    def unpack(self, packed):
+        k, t = packed
+        if k not in self.consumer:
+            self.consumer[k] = _current_node()
+        return t
+
+
+def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16):
+    """Trace one step — ``forward_fn()`` returns the loss, backward runs here — into a CompGraph.
+
+    Returns (graph, meta) where meta maps graph ids back to pack indices and
+    autograd-node ranks.  The traced step's gradients are left in place.
+    """
+    cap = _Capture()
+    with torch.autograd.graph.saved_tensors_hooks(cap.pack, cap.unpack):
+        loss = forward_fn()
+    root = loss.grad_fn
+    nodes = _walk(root)
+    loss.backward()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+
+    accs = [n for n in nodes if _is_accumulate(n)]
+    ops = sorted((n for n in nodes if not _is_accumulate(n)), key=lambda n: n._sequence_nr())
+    seq0 = ops[0]._sequence_nr() if ops else 0
+    rank = {n: n._sequence_nr() - seq0 for n in ops}
+
+    # ids: variables first (params in pack/encounter order, then inputs), then F, B, U ops
+    gnodes, gedges, gtensors = [], [], []
+
+    def new_tensor(producer_id, nbytes):
+        tid = len(gtensors)
+        gtensors.append(TensorSpec(tid, producer_id, int(nbytes)))
+        return tid
+
+    var_of_acc = {}
+    for i, a in enumerate(accs):
+        nid = len(gnodes)
+        gnodes.append(variable_node(nid, f"param_{i}", scope="params"))
+        var_of_acc[a] = (nid, new_tensor(nid, 0))
+    input_var = len(gnodes)
+    gnodes.append(variable_node(input_var, "input", scope="inputs"))
+    input_t = new_tensor(input_var, 0)
+    seed_var = len(gnodes)
+    gnodes.append(variable_node(seed_var, "grad_seed", scope="inputs"))
+    seed_t = new_tensor(seed_var, 0)
+
+    F, B = {}, {}
+    main_out = {}
+    for n in ops:
+        nid = len(gnodes)
+        gnodes.append(compute_node(nid, _fwd_name(n), scope="model", phase=Phase.FORWARD))
+        F[n] = nid
+        main_out[n] = new_tensor(nid, 0)
+    for n in ops:
+        for nxt, _ in n.next_functions:
+            if nxt is None:
+                gedges.append(EdgeRec(input_var, F[n], EdgeAction.READ, input_t))
+            elif _is_accumulate(nxt):
+                v, vt = var_of_acc[nxt]
+                gedges.append(EdgeRec(v, F[n], EdgeAction.READ, vt))
+            else:
+                gedges.append(EdgeRec(F[nxt], F[n], EdgeAction.READ, main_out[nxt]))
+        if not n.next_functions:
+            gedges.append(EdgeRec(input_var, F[n], EdgeAction.READ, input_t))
+
+    # distinct saved tensors; producer = grad_fn, or the saving op itself for
+    # non-differentiable outputs (indices, saved statistics)
+    by_key = {}
+    saved = []
+    pack_saved = []
+    for k, (key, nbytes, grad_fn, is_leaf, req, is_param) in enumerate(cap.packs):
+        consumer = cap.consumer.get(k)
+        if consumer is None or consumer not in rank:
+            pack_saved.append(-1)
+            continue
+        s = by_key.get(key)
+        if s is None:
+            if is_param or (is_leaf and req):
+                producer = None
+            elif grad_fn is not None and grad_fn in rank:
+                producer = grad_fn
+            elif is_leaf:
+                producer = None  # a step input
+            else:
+                producer = "self"
+            s = _Saved(len(saved), nbytes, producer, is_param)
+            by_key[key] = s
+            saved.append(s)
+        s.packs.append(k)
+        pack_saved.append(s.tid)
+
+    for n in reversed(ops):  # backward ops in reverse creation order
+        nid = len(gnodes)
+        gnodes.append(compute_node(nid, n.name(), scope="grads", phase=Phase.BACKWARD))
+        B[n] = nid
+    grad_out = {n: new_tensor(B[n], 0) for n in ops}
+    if root in B:
+        gedges.append(EdgeRec(seed_var, B[root], EdgeAction.READ, seed_t))
+    acc_grad = {}
+    for n in ops:
+        for nxt, _ in n.next_functions:
+            if nxt is None:
+                continue
+            if _is_accumulate(nxt):
+                acc_grad.setdefault(nxt, []).append(n)
+            else:
+                gedges.append(EdgeRec(B[n], B[nxt], EdgeAction.READ, grad_out[n]))
+
+    saved_tensor_id = {}
+    seen_edge = set()
+    for k, si in enumerate(pack_saved):
+        if si < 0:
+            continue
+        s = saved[si]
+        cons = cap.consumer[k]
+        if s.producer is None:
+            continue  # params and inputs stay resident (variables are never swapped)
+        prod = cons if s.producer == "self" else s.producer
+        if s.producer != "self" and s.nbytes == 0:
+            continue
+        tid = saved_tensor_id.get(si)
+        if tid is None:
+            if s.producer != "self" and prod in main_out and gtensors[main_out[prod]].size_bytes == 0:
+                tid = main_out[prod]
+                gtensors[tid] = TensorSpec(tid, F[prod], s.nbytes)
+            else:
+                tid = new_tensor(F[prod], s.nbytes)
+            saved_tensor_id[si] = tid
+        if s.nbytes < min_swap_bytes:
+            continue  # tiny tensors stay on the device; no candidate edge
+        e = EdgeRec(F[prod], B[cons], EdgeAction.READ, tid)
+        if e not in seen_edge:
+            seen_edge.add(e)
+            gedges.append(e)
+
+    for a, users in acc_grad.items():
+        v, vt = var_of_acc[a]
+        uid = len(gnodes)
+        gnodes.append(compute_node(uid, "sgd", scope="optimizer", phase=Phase.UPDATE))
+        gedges.append(EdgeRec(v, uid, EdgeAction.READ, vt))
+        for u in users:
+            gedges.append(EdgeRec(B[u], uid, EdgeAction.READ, grad_out[u]))
+        upd = new_tensor(uid, 0)
+        gedges.append(EdgeRec(uid, v, EdgeAction.UPDATE, upd))
+
+    g = CompGraph(gnodes, gedges, gtensors)
+    meta = {
+        "n_packs": len(cap.packs),
+        "pack_saved": pack_saved,
+        "saved": saved,
+        "saved_tensor_id": saved_tensor_id,
+        "F": {F[n]: rank[n] for n in ops},
+        "B": {B[n]: rank[n] for n in ops},
+        "consumer_rank": {k: rank.get(c) for k, c in cap.consumer.items()},
+    }
+    return g, meta
+
+
+def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int) -> SwapPlan:
+    """Rewrite the captured graph and map swap-ins back onto pack indices / nodes."""
+    t0 = time.perf_counter()
+    out, rep = rewrite(g, cfg)
+    dt = time.perf_counter() - t0
+    tid_to_saved = {tid: si for si, tid in meta["saved_tensor_id"].items()}
+    B = meta["B"]
+    F = meta["F"]
+    swapped_tids = {tid for _, _, tid in rep.edges_rewritten}
+    pack_saved = meta["pack_saved"]
+    saved_info = [_SavedInfo(s.tid, s.nbytes, meta["saved_tensor_id"].get(s.tid) in swapped_tids)
+                  for s in meta["saved"]]
+
+    # swap-in nodes -> groups
+    groups = []
+    pack_group = {}
+    triggers: dict[int, list] = {}
+    bwd_start, eager = [], []
+    ctrl_of = {e.dst: e.src for e in out.edges if e.action is EdgeAction.CONTROL}
+    for n in out.nodes:
+        if n.kind is not NodeKind.SWAP_IN:
+            continue
+        src = next(e for e in out.in_edges(n.id) if e.action is EdgeAction.READ)
+        so = src.src
+        orig = next(e for e in out.in_edges(so) if e.action is EdgeAction.READ).tensor
+        si = tid_to_saved[orig]
+        consumers = {B[e.dst] for e in out.out_edges(n.id) if e.action is EdgeAction.READ}
+        packs = [k for k in meta["saved"][si].packs if meta["consumer_rank"].get(k) in consumers]
+        c = ctrl_of.get(n.id)
+        if c is None:
+            kind, trig = "eager", None
+        elif c in B:
+            kind, trig = "backward", B[c]
+        else:
+            kind, trig = "forward->bwd-start", None
+        grp = SwapGroup(len(groups), si, packs, trig, kind)
+        groups.append(grp)
+        for k in packs:
+            pack_group[k] = grp.gid
+        if kind == "backward":
+            triggers.setdefault(trig, []).append(grp.gid)
+        elif kind == "eager":
+            eager.append(grp.gid)
+        else:
+            bwd_start.append(grp.gid)
+    # packs of a swapped tensor whose consumer edge was not rewritten keep the tensor
+    pack_is_swapped = [k in pack_group for k in range(meta["n_packs"])]
+    swapped_bytes = sum(s.nbytes for s in saved_info if s.swapped)
+    plan = SwapPlan(
+        graph=g, rewritten=out, report=rep, n_packs=meta["n_packs"],
+        pack_saved=[si if (si >= 0 and pack_is_swapped[k]) else -1 for k, si in enumerate(pack_saved)],
+        saved=saved_info, groups=groups, pack_group=pack_group, triggers=triggers,
+        bwd_start_groups=bwd_start, eager_groups=eager,
+        swapped_bytes_per_step=swapped_bytes,
+        saved_bytes_per_step=sum(s.nbytes for s in saved_info),
+        capture_batch=capture_batch, rewrite_seconds=dt)
+    _ = F
+    return plan
+
+
+def _issuer(issue, gids):
+    def hook(grad_inputs, grad_outputs):
+        for gid in gids:
+            issue(gid)
+        return None
+    return hook
+
+
+class _SwapRef:
+    """What autograd keeps instead of a swapped tensor."""
+
+    __slots__ = ("k",)
+
+    def __init__(self, k):
+        self.k = k
+
+
+class SwapExecutor:
+    """Runs training steps under a :class:`SwapPlan` on one device."""
+
+    def __init__(self, ctx: rt.Context, plan: SwapPlan, codec: str | dict = "ce"):
+        self.ctx = ctx
+        self.plan = plan
+        self.codec = codec
+        self.last_stats = {}
+
+    def _codec_for(self, si: int, t) -> str:
+        if isinstance(self.codec, str):
+            return self.codec
+        return self.codec.get(si, "ce")
+
+    def run(self, forward_fn):
+        """``forward_fn()`` runs forward and returns the loss; backward happens here."""
+        plan, ctx = self.plan, self.ctx
+        k_counter = [0]
+        handles: dict[int, rt.SwapHandle] = {}     # saved idx -> host copy
+        group_tensor: dict[int, torch.Tensor] = {}
+        group_waited: dict[int, int] = {}
+        group_left = {g.gid: len(g.packs) for g in plan.groups}
+        issued: set[int] = set()
+        stream_of = torch.cuda.current_stream
+
+        def issue(gid):
+            if gid in issued:
+                return
+            grp = plan.groups[gid]
+            h = handles.get(grp.saved)
+            if h is None:
+                return  # its swap-out never happened (structure changed); unpack will fail loudly
+            issued.add(gid)
+            group_tensor[gid] = ctx.swap_in(h, trigger_stream=stream_of())
+
+        def pack(t):
+            k = k_counter[0]
+            k_counter[0] = k + 1
+            si = plan.pack_saved[k] if k < plan.n_packs else -1
+            if si < 0:
+                return t
+            h = handles.get(si)
+            if h is None:
+                h = ctx.swap_out(t, self._codec_for(si, t), stream_of())
+                handles[si] = h
+                for gid in plan.eager_groups:
+                    if plan.groups[gid].saved == si:
+                        issue(gid)
+            return _SwapRef(k)
+
+        def unpack(obj):
+            if not isinstance(obj, _SwapRef):
+                return obj
+            gid = plan.pack_group[obj.k]
+            if gid not in issued:
+                issue(gid)  # control op did not fire (e.g. pruned branch): fetch now
+            t = group_tensor.get(gid)
+            if t is None:
+                # unpacked again after the group was released: fetch once more
+                issued.discard(gid)
+                issue(gid)
+                t = group_tensor[gid]
+            ctx.wait(handles[plan.groups[gid].saved], stream_of())
+            group_left[gid] -= 1
+            if group_left[gid] <= 0:
+                group_tensor.pop(gid, None)  # the consumer node holds it until it finishes
+            return t
+
+        with torch.autograd.graph.saved_tensors_hooks(pack, unpack):
+            loss = forward_fn()
+        if k_counter[0] != plan.n_packs:
+            raise RuntimeError(f"step saved {k_counter[0]} tensors but the plan was captured with "
+                               f"{plan.n_packs}; re-capture the plan for this model/step")
+        # hook the control ops of this step's graph
+        hooks = []
+        if plan.triggers:
+            ops = sorted((n for n in _walk(loss.grad_fn) if not _is_accumulate(n)),
+                         key=lambda n: n._sequence_nr())
+            seq0 = ops[0]._sequence_nr()
+            for n in ops:
+                gids = plan.triggers.get(n._sequence_nr() - seq0)
+                if gids:
+                    hooks.append(n.register_hook(_issuer(issue, gids)))
+        for gid in plan.bwd_start_groups:
+            issue(gid)
+        loss.backward()
+        for h in hooks:
+            h.remove()
+        for h in handles.values():
+            ctx.release(h)
+        group_tensor.clear()
+        return loss
+
+
+class LMS:
+    """TFLMS for a PyTorch training step: capture once, rewrite, then train with swapping.
+
+    ``LMS(model, loss_fn, optimizer, RewriteConfig(...), ctx)`` mirrors the
+    paper's usage (``LMS(...).run(graph)``, PAPER §5): the rewrite knobs are
+    exactly the reference's ``RewriteConfig``.
+    """
+
+    def __init__(self, model, loss_fn, optimizer, cfg: RewriteConfig, ctx: rt.Context,
+                 codec="ce", min_swap_bytes: int = 1 << 16):
+        self.model, self.loss_fn, self.optimizer = model, loss_fn, optimizer
+        self.cfg = cfg
+        self.ctx = ctx
+        self.codec = codec
+        self.min_swap_bytes = min_swap_bytes
+        self.plan: SwapPlan | None = None
+        self.graph = None
+        self.meta = None
+        self._exec = None
+
+    def capture(self, x, y):
+        """Trace one step at (x, y) — no optimizer update — and build the swap plan."""
+        self.optimizer.zero_grad(set_to_none=True)
+        self.graph, self.meta = capture_graph(lambda: self.loss_fn(self.model(x), y), self.min_swap_bytes)
+        self.optimizer.zero_grad(set_to_none=True)
+        self.replan(self.cfg)
+        return self.plan
+
+    def replan(self, cfg: RewriteConfig):
+        """Re-run the rewrite with new knobs on the captured graph (no re-trace)."""
+        self.cfg = cfg
+        self.plan = build_plan(self.graph, self.meta, cfg, 0)
+        self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
+        return self.plan
+
+    def step(self, x, y):
+        """One swapped training step; returns the loss tensor (on device)."""
+        self.optimizer.zero_grad(set_to_none=True)
+        loss = self._exec.run(lambda: self.loss_fn(self.model(x), y))
+        self.optimizer.step()
+        return loss

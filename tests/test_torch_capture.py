@@ -1,0 +1,58 @@
+"""Capture adapter (PyTorch autograd step -> CompGraph) on CPU.
+
+The captured graph must be valid under the reference's ``validate`` rules,
+carry forward/backward/update phases, and the reference rewrite must find the
+saved activations as forward->backward candidates.
+"""
+
+import torch
+
+from paper_1807_02037_b200 import EdgeAction, NodeKind, Phase, RewriteConfig, validate
+from paper_1807_02037_b200.torch_lms import build_plan, capture_graph
+
+
+def _model():
+    torch.manual_seed(0)
+    return torch.nn.Sequential(
+        torch.nn.Conv2d(3, 8, 3, padding=1), torch.nn.BatchNorm2d(8), torch.nn.ReLU(),
+        torch.nn.MaxPool2d(2),
+        torch.nn.Conv2d(8, 16, 3, padding=1), torch.nn.ReLU(),
+        torch.nn.Flatten(), torch.nn.Linear(16 * 8 * 8, 10))
+
+
+def test_capture_is_valid_training_graph():
+    m = _model()
+    x = torch.randn(4, 3, 16, 16)
+    y = torch.randint(0, 10, (4,))
+    g, meta = capture_graph(lambda: torch.nn.functional.cross_entropy(m(x), y), min_swap_bytes=0)
+    assert validate(g) == []
+    phases = {n.phase for n in g.nodes if not n.parameterized}
+    assert phases == {Phase.FORWARD, Phase.BACKWARD, Phase.UPDATE}
+    n_params = sum(1 for _ in m.parameters())
+    assert sum(1 for n in g.nodes if n.kind is NodeKind.VARIABLE) == n_params + 2
+    fwd_bwd = [e for e in g.edges if e.action is EdgeAction.READ
+               and g.node(e.src).phase is Phase.FORWARD and g.node(e.dst).phase is Phase.BACKWARD]
+    assert len(fwd_bwd) >= 6  # conv inputs, bn input, relu outputs, pool indices, ...
+    plan = build_plan(g, meta, RewriteConfig(), capture_batch=4)
+    assert plan.report.tensors_swapped == len({e.tensor for e in fwd_bwd})
+    assert len(plan.groups) == plan.report.swap_ins_added
+    # every swapped pack is served by exactly one swap-in group
+    served = sorted(k for grp in plan.groups for k in grp.packs)
+    assert served == sorted(set(served))
+    assert all(plan.pack_saved[k] >= 0 for k in served)
+    kinds = {grp.trigger_kind for grp in plan.groups}
+    assert "backward" in kinds
+
+
+def test_n_tensors_and_fusion_knobs_apply():
+    m = _model()
+    x = torch.randn(2, 3, 16, 16)
+    y = torch.randint(0, 10, (2,))
+    g, meta = capture_graph(lambda: torch.nn.functional.cross_entropy(m(x), y), min_swap_bytes=0)
+    p3 = build_plan(g, meta, RewriteConfig(n_tensors=3), capture_batch=2)
+    assert p3.report.tensors_swapped == 3
+    pf = build_plan(g, meta, RewriteConfig(fuse_swapins=True, swapin_fuse_distance=100), capture_batch=2)
+    pn = build_plan(g, meta, RewriteConfig(), capture_batch=2)
+    assert len(pf.groups) <= len(pn.groups)
+    pd = build_plan(g, meta, RewriteConfig(ctrld_strategy="direct_order", lb=2), capture_batch=2)
+    assert pd.report.control_edges_added > 0

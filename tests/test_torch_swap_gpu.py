@@ -1,0 +1,78 @@
+"""PyTorch training under swapping vs without (north-star parity rule 2).
+
+Losses and every parameter after several SGD steps must agree within fp32
+relative tolerance 1e-5 (bit-equal is expected: swapping is a copy and the
+kernels are deterministic).  Covers each transfer codec, fused swap-ins,
+both control strategies and the n_tensors cap.
+"""
+
+import copy
+
+import pytest
+import torch
+
+from paper_1807_02037_b200 import RewriteConfig
+from paper_1807_02037_b200.torch_lms import LMS
+
+pytestmark = pytest.mark.gpu
+
+
+def _net():
+    torch.manual_seed(0)
+    return torch.nn.Sequential(
+        torch.nn.Conv2d(3, 32, 3, padding=1), torch.nn.BatchNorm2d(32), torch.nn.ReLU(inplace=True),
+        torch.nn.MaxPool2d(2),
+        torch.nn.Conv2d(32, 64, 3, padding=1), torch.nn.BatchNorm2d(64), torch.nn.ReLU(inplace=True),
+        torch.nn.Conv2d(64, 64, 3, padding=1), torch.nn.ReLU(),
+        torch.nn.AdaptiveAvgPool2d(1), torch.nn.Flatten(), torch.nn.Linear(64, 10)).cuda()
+
+
+def _train(model, stepper, steps, x, y):
+    losses = []
+    for i in range(steps):
+        losses.append(float(stepper(x[i], y[i])))
+    return losses
+
+
+@pytest.mark.parametrize("codec,cfg", [
+    ("ce", RewriteConfig()),
+    ("sm", RewriteConfig(lb=2)),
+    ("zvc", RewriteConfig(fuse_swapins=True, swapin_fuse_distance=2)),
+    ("ce", RewriteConfig(ctrld_strategy="direct_order", lb=3, n_tensors=4)),
+])
+def test_swapped_training_matches_plain(lms_ctx, codec, cfg):
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    base = _net()
+    swp = copy.deepcopy(base)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(3, 16, 3, 32, 32, device="cuda", generator=gen)
+    y = torch.randint(0, 10, (3, 16), device="cuda", generator=gen)
+    loss_fn = torch.nn.functional.cross_entropy
+
+    opt_a = torch.optim.SGD(base.parameters(), lr=0.1, momentum=0.9)
+
+    def plain(xb, yb):
+        opt_a.zero_grad(set_to_none=True)
+        loss = loss_fn(base(xb), yb)
+        loss.backward()
+        opt_a.step()
+        return loss
+
+    opt_b = torch.optim.SGD(swp.parameters(), lr=0.1, momentum=0.9)
+    lms = LMS(swp, loss_fn, opt_b, cfg, lms_ctx, codec=codec, min_swap_bytes=0)
+    lms.capture(x[0], y[0])
+    # capture ran forward/backward without an optimizer step; reset BN stats drift
+    swp.load_state_dict(base.state_dict())
+    assert lms.plan.report.tensors_swapped > 0
+
+    la = _train(base, plain, 3, x, y)
+    lb = _train(swp, lms.step, 3, x, y)
+    torch.cuda.synchronize()
+    for a, b in zip(la, lb):
+        assert abs(a - b) <= 1e-5 * abs(a)
+    for (n, pa), pb in zip(base.named_parameters(), swp.parameters()):
+        err = (pa - pb).norm() / pa.norm().clamp_min(1e-30)
+        assert err <= 1e-5, n
+    st = lms_ctx.stats()
+    assert st["n_swap_out"] > 0 and st["n_swap_in"] > 0
