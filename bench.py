@@ -169,12 +169,13 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a GPU (no CPU fallback)")
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     budget = int(args.budget_gib * GIB) if not args.quick else 4 * GIB
 
+    # the pool must own PyTorch's allocator before anything lazily initialises CUDA
     ctx = rt.Context(device=local, device_reserve=budget, host_chunk=4 * GIB, timing=True)
     rt.install_allocator(ctx)
+    torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)

@@ -955,7 +955,7 @@ int lms_unpack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, con
 size_t lms_zvc_bound(size_t nwords) { return zvc_bound(nwords); }
 
 int lms_zvc_encode(lms_ctx* c, const void* src, size_t nwords, void* dst, void* stream) {
-  if (!c || !src || !dst) return fail(LMS_E_INVALID, "null argument");
+  if (!c || (!src && nwords) || !dst) return fail(LMS_E_INVALID, "null argument");
   if (reinterpret_cast<uintptr_t>(src) % 16 || reinterpret_cast<uintptr_t>(dst) % 16)
     return fail(LMS_E_INVALID, "zvc buffers must be 16-byte aligned");
   std::lock_guard<std::mutex> g(c->mu);
@@ -964,7 +964,8 @@ int lms_zvc_encode(lms_ctx* c, const void* src, size_t nwords, void* dst, void* 
 }
 
 int lms_zvc_decode(lms_ctx* c, const void* enc, size_t nwords, void* dst, void* stream) {
-  if (!c || !enc || !dst) return fail(LMS_E_INVALID, "null argument");
+  if (!c || !enc || (!dst && nwords)) return fail(LMS_E_INVALID, "null argument");
+  if (nwords == 0) return LMS_OK;
   return launch_zvc_decode(c, static_cast<const char*>(enc), nwords, static_cast<uint32_t*>(dst),
                            static_cast<cudaStream_t>(stream));
 }

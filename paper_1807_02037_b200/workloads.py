@@ -1,19 +1,24 @@
 """Interpreter-vocabulary training graphs (BASELINE config 1).
 
 ``ffchain(L, N)`` is a feed-forward chain of ``L`` N×N ``matmul`` layers
-with a backward pass in the same vocabulary and one ``sub`` update per
-weight — the graph the reference CPU executor (``interp.py:58-190``) and the
-GPU executor both run.  Shape of one step:
+with its backward pass written in the same vocabulary and one ``sub`` update
+per weight — the graph the reference CPU executor (``interp.py:58-190``) and
+the GPU executor both run.  The backward mirrors real autodiff: each
+activation is re-read by two backward ops, and the op that consumes layer
+i+1's activation is an ancestor of layer i's backward, so the chain-rule
+strategy finds control ops right behind the consumer (PAPER §4.3, Alg. 2).
 
     forward   h[i+1] = matmul(h[i], W[i])            i = 0..L-1, h[0] = x
     backward  g[L]   = neg(h[L])
-              dW[i]  = mul(g[i+1], h[i+1])           elementwise
-              g[i]   = matmul(g[i+1], W[i])          i = L-1..1
-    update    W[i]  <- sub(W[i], dW[i])              update edge into W[i]
+              d[i]   = mul(g[i+1], h[i+1])            "activation derivative"
+              dW[i]  = matmul(h[i], d[i])
+              g[i]   = matmul(d[i], W[i])             i = L-1..1
+    update    W[i]  <- sub(W[i], dW[i])               update edge into W[i]
 
-Every activation h[1..L] is read forward->backward, so a default rewrite
-swaps all ``L`` of them.  Inputs: ``numpy.random.default_rng(seed)``
-standard normal × ``scale`` per variable.
+A default rewrite swaps h[1..L] (8 tensors at L=8) with two swap-ins each.
+Operand order follows the interpreter's rule (ascending origin tensor id).
+Inputs: ``numpy.random.default_rng(seed)`` standard normal, weights scaled
+by 1/sqrt(N) so values stay O(1) through the chain in fp32.
 """
 
 from __future__ import annotations
@@ -32,46 +37,41 @@ def ffchain(layers: int, n: int, elem_bytes: int = 4) -> CompGraph:
     edges: list[EdgeRec] = []
     tensors: list[TensorSpec] = []
 
-    def node(name, scope, kind=NodeKind.COMPUTE, phase=Phase.UNKNOWN, size=nbytes):
+    def node(name, scope, kind=NodeKind.COMPUTE, phase=Phase.UNKNOWN):
         nid = len(nodes)
         param = kind in (NodeKind.VARIABLE, NodeKind.CONSTANT)
-        nodes.append(OpNode(nid, name, scope, kind, param, phase, "acc:0",
-                            0.0 if param else 1.0))
-        tensors.append(TensorSpec(len(tensors), nid, size, dtype))
+        nodes.append(OpNode(nid, name, scope, kind, param, phase, "acc:0", 0.0 if param else 1.0))
+        tensors.append(TensorSpec(len(tensors), nid, nbytes, dtype))
         return nid, len(tensors) - 1
 
-    def read(tid, dst):
-        edges.append(EdgeRec(tensors[tid].producer, dst, EdgeAction.READ, tid))
+    def op(name, scope, phase, *reads):
+        nid, tid = node(name, scope, phase=phase)
+        for r in reads:
+            edges.append(EdgeRec(tensors[r].producer, nid, EdgeAction.READ, r))
+        return nid, tid
 
-    _, h = node("x", "input", NodeKind.VARIABLE)
-    weights = []
+    _, x = node("x", "input", NodeKind.VARIABLE)
+    weights = [node(f"W{i}", f"params/l{i}", NodeKind.VARIABLE) for i in range(layers)]
+    h = [x]
     for i in range(layers):
-        weights.append(node(f"W{i}", f"params/l{i}", NodeKind.VARIABLE))
-    acts = [h]
-    for i in range(layers):
-        nid, h = node("matmul", f"model/l{i}", phase=Phase.FORWARD)
-        read(acts[-1], nid)
-        read(weights[i][1], nid)
-        acts.append(h)
-    nid, g = node("neg", "grads/top", phase=Phase.BACKWARD)
-    read(acts[layers], nid)
+        h.append(op("matmul", f"model/l{i}", Phase.FORWARD, h[i], weights[i][1])[1])
+    g = op("neg", "grads/top", Phase.BACKWARD, h[layers])[1]
     for i in reversed(range(layers)):
-        nid, dw = node("mul", f"grads/l{i}/dw", phase=Phase.BACKWARD)
-        read(g, nid)
-        read(acts[i + 1], nid)
-        unid, upd = node("sub", f"optimizer/l{i}", phase=Phase.UPDATE)
-        read(weights[i][1], unid)
-        read(dw, unid)
-        edges.append(EdgeRec(unid, weights[i][0], EdgeAction.UPDATE, upd))
+        d = op("mul", f"grads/l{i}/act", Phase.BACKWARD, g, h[i + 1])[1]
+        dw = op("matmul", f"grads/l{i}/dw", Phase.BACKWARD, h[i], d)[1]
         if i > 0:
-            nid, g2 = node("matmul", f"grads/l{i}/dx", phase=Phase.BACKWARD)
-            read(g, nid)
-            read(weights[i][1], nid)
-            g = g2
+            g = op("matmul", f"grads/l{i}/dx", Phase.BACKWARD, d, weights[i][1])[1]
+        unid, upd = op("sub", f"optimizer/l{i}", Phase.UPDATE, weights[i][1], dw)
+        edges.append(EdgeRec(unid, weights[i][0], EdgeAction.UPDATE, upd))
     return CompGraph(nodes, edges, tensors)
 
 
-def ffchain_inputs(g: CompGraph, n: int, seed: int = 0, scale: float = 0.1) -> dict[str, np.ndarray]:
+def ffchain_inputs(g: CompGraph, n: int, seed: int = 0) -> dict[str, np.ndarray]:
     """float64 N×N per variable, drawn in ascending node id order."""
     rng = np.random.default_rng(seed)
-    return {nd.name: rng.standard_normal((n, n)) * scale for nd in g.nodes if nd.parameterized}
+    out = {}
+    for nd in g.nodes:
+        if nd.parameterized:
+            scale = 1.0 if nd.name == "x" else 1.0 / np.sqrt(n)
+            out[nd.name] = rng.standard_normal((n, n)) * scale
+    return out
