@@ -330,6 +330,13 @@ def main():
             if not is_oom(e):
                 raise
             ok = False
+            log(f"[bench] OOM detail: {str(e)[:300]}")
+            log(f"[bench] pool: { {k: v for k, v in ctx.stats().items() if k.startswith('device')} }")
+        log(f"[bench] plan: {plan.summary()}")
+        kinds = {}
+        for grp in plan.groups:
+            kinds[grp.trigger_kind] = kinds.get(grp.trigger_kind, 0) + 1
+        log(f"[bench] trigger kinds: {kinds}")
         attempts.append({"n_tensors": cfg.n_tensors, "ok": ok})
         ok = agree(1.0 if ok else 0.0) > 0.5
         if ok:

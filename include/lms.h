@@ -71,8 +71,11 @@ typedef struct {
 } lms_config_t;
 
 typedef struct {
-  uint64_t device_in_use, device_peak, device_reserved, device_limit;
+  uint64_t device_in_use, device_peak;         /* live block bytes (the model's residency) */
+  uint64_t device_reserved, device_limit;      /* VA reserved; physical budget */
   uint64_t device_largest_free, device_deferred_bytes;
+  uint64_t device_mapped, device_mapped_peak;  /* physical pages actually backing blocks */
+  uint64_t n_map, n_unmap, n_reclaims;
   uint64_t host_in_use, host_peak, host_reserved;
   uint64_t n_alloc, n_free, n_oom, n_deferred_frees, n_cross_stream_waits;
   uint64_t n_swap_out, n_swap_in, n_handles_live;

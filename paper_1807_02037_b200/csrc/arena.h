@@ -21,11 +21,12 @@ struct Block {
   Block* prev = nullptr;
   Block* next = nullptr;
   void* tag = nullptr;  // owner-defined (last-use stream for device blocks)
+  class Arena* owner = nullptr;
 };
 
 class Arena {
  public:
-  static constexpr size_t kAlign = 512;
+  static constexpr size_t kAlign = 512;  // default granularity
 
   Arena() = default;
   Arena(const Arena&) = delete;
@@ -34,11 +35,12 @@ class Arena {
 
   // `fresh` tags never-used space: it merges with any neighbour and adopts
   // the neighbour's tag, since it has no pending work on any stream.
-  void init(char* base, size_t capacity, void* fresh = nullptr) {
+  void init(char* base, size_t capacity, void* fresh = nullptr, size_t align = kAlign) {
     clear();
+    align_ = align;
     fresh_ = fresh;
     base_ = base;
-    cap_ = capacity - capacity % kAlign;
+    cap_ = capacity - capacity % align_;
     if (cap_ == 0) return;
     Block* b = new Block();
     b->off = 0;
@@ -49,11 +51,13 @@ class Arena {
   }
 
   static size_t round(size_t n) { return n == 0 ? kAlign : (n + kAlign - 1) / kAlign * kAlign; }
+  size_t round_up(size_t n) const { return n == 0 ? align_ : (n + align_ - 1) / align_ * align_; }
+  size_t align() const { return align_; }
 
   // Best fit with a `tag` preference: among free blocks of the smallest
   // adequate size class, the first whose tag matches wins, else the smallest.
   Block* alloc(size_t size, void* tag_pref = nullptr, bool require_tag = false) {
-    size = round(size);
+    size = round_up(size);
     auto it = free_.lower_bound({size, nullptr});
     Block* pick = nullptr;
     if (tag_pref != nullptr || require_tag) {
@@ -68,7 +72,7 @@ class Arena {
       pick = it->second;
     }
     free_.erase(it);
-    if (pick->size - size >= kAlign) {
+    if (pick->size - size >= align_) {
       Block* rest = new Block();
       rest->off = pick->off + size;
       rest->size = pick->size - size;
@@ -81,6 +85,7 @@ class Arena {
       free_.insert({rest->size, rest});
     }
     pick->free = false;
+    pick->owner = this;
     used_ += pick->size;
     if (used_ > peak_) peak_ = used_;
     live_[pick->off] = pick;
@@ -167,6 +172,10 @@ class Arena {
   void for_each_free(F&& f) const {
     for (auto& kv : free_) f(kv.second);
   }
+  template <class F>
+  void for_each_live(F&& f) const {
+    for (auto& kv : live_) f(kv.second);
+  }
 
  private:
   void clear() {
@@ -192,6 +201,7 @@ class Arena {
   };
 
   char* base_ = nullptr;
+  size_t align_ = kAlign;
   void* fresh_ = nullptr;
   size_t cap_ = 0;
   Block* head_ = nullptr;

@@ -29,6 +29,7 @@
 #include "../../include/lms.h"
 #include "arena.h"
 #include "kernels.cuh"
+#include "vmm_pool.h"
 
 namespace lms {
 
@@ -130,10 +131,11 @@ struct lms_ctx {
   void* home = nullptr;  // compute stream (immediate reuse)
   EventPool events;
 
-  // device arena
-  char* dev_base = nullptr;
-  Arena dev;
+  // device pool: VA arenas over CUDA virtual memory, physical pages under the budget
+  VmmPool* vmm = nullptr;
   size_t limit = 0;
+  size_t alloc_bytes = 0, alloc_peak = 0;   // live block bytes (the model's residency)
+  uint64_t n_reclaims = 0;
   std::unordered_map<Block*, std::vector<SharedEv*>> holds;
   std::vector<Block*> deferred;
   size_t deferred_bytes = 0;
@@ -194,6 +196,13 @@ bool holds_clear(lms_ctx* c, Block* b) {
   return false;
 }
 
+void release_block(lms_ctx* c, Block* b) {
+  Arena& ar = *b->owner;
+  c->vmm->pin(ar, b, -1);
+  c->alloc_bytes -= b->size;
+  ar.release(b);
+}
+
 void reap_deferred(lms_ctx* c, bool block) {
   size_t w = 0;
   for (size_t i = 0; i < c->deferred.size(); ++i) {
@@ -205,7 +214,7 @@ void reap_deferred(lms_ctx* c, bool block) {
     }
     if (holds_clear(c, b)) {
       c->deferred_bytes -= b->size;
-      c->dev.release(b);
+      release_block(c, b);
     } else {
       c->deferred[w++] = b;
     }
@@ -217,67 +226,84 @@ void stream_wait_on(lms_ctx* c, void* waiter, void* owner) {
   cudaEvent_t e = c->events.get();
   cudaEventRecord(e, static_cast<cudaStream_t>(owner));
   cudaStreamWaitEvent(static_cast<cudaStream_t>(waiter), e, 0);
-  c->events.put(e);  // recycled after the wait is enqueued: safe, re-record only later
+  c->events.put(e);  // the wait captured the record; the event may be re-recorded later
   c->st.n_cross_stream_waits++;
 }
 
-int ensure_arena(lms_ctx* c) {
-  if (c->dev_base) return LMS_OK;
-  size_t want = c->cfg.device_reserve;
-  if (want == 0) {
+int ensure_pool(lms_ctx* c) {
+  if (c->vmm) return LMS_OK;
+  size_t limit = c->cfg.device_limit ? c->cfg.device_limit : c->cfg.device_reserve;
+  if (limit == 0) {
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
-    want = fr > (size_t(2) << 30) ? fr - (size_t(2) << 30) : fr / 2;
-    if (c->cfg.device_limit && c->cfg.device_limit < want) want = c->cfg.device_limit;
+    limit = fr > (size_t(2) << 30) ? fr - (size_t(2) << 30) : fr / 2;
   }
-  void* p = nullptr;
-  CK(cudaMalloc(&p, want));
-  c->dev_base = static_cast<char*>(p);
-  c->dev.init(c->dev_base, want, kFresh);
-  if (c->limit == 0 || c->limit > c->dev.capacity()) c->limit = c->dev.capacity();
+  auto* v = new VmmPool();
+  std::string err;
+  if (!v->init(c->device, limit, 4 * limit, kFresh, &err)) {
+    delete v;
+    return fail(LMS_E_CUDA, "device pool: " + err);
+  }
+  c->vmm = v;
+  c->limit = v->limit_bytes();
   return LMS_OK;
 }
 
-// returns LMS_OK and *out, or LMS_E_OOM
+// returns LMS_OK and *out, or LMS_E_OOM.  Escalation when the budget is
+// short: (0) as is, (1) wait for deferred frees (pending swap-out copies),
+// (2) drain the device, merge stream-split ranges and unmap idle cached pages.
 int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
-  int rc = ensure_arena(c);
+  int rc = ensure_pool(c);
   if (rc) return rc;
-  size_t need = Arena::round(size);
+  VmmPool& v = *c->vmm;
+  Arena& ar = v.arena_for(size);
   reap_deferred(c, false);
+  std::string err;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if (c->dev.used() + need <= c->limit) {
-      Block* b = c->dev.alloc(need, stream);
-      if (b) {
-        void* prev = b->tag;
-        if (prev != kFresh && prev != stream) stream_wait_on(c, stream, prev);
-        b->tag = stream;
-        c->st.n_alloc++;
-        *out = c->dev_base + b->off;
-        return LMS_OK;
-      }
-    }
-    if (attempt == 0) {
-      if (c->deferred.empty()) attempt = 1; else reap_deferred(c, true);
-    }
     if (attempt == 1) {
-      // merge blocks split by stream tags: after a device sync nothing is pending
+      if (c->deferred.empty()) continue;
+      reap_deferred(c, true);
+    }
+    if (attempt == 2) {
       cudaDeviceSynchronize();
       reap_deferred(c, true);
-      c->dev.retag_all_free(kFresh);
+      v.small_.retag_all_free(kFresh);
+      v.large_.retag_all_free(kFresh);
     }
+    Block* b = ar.alloc(size, stream);
+    if (!b) continue;
+    v.pin(ar, b, +1);
+    size_t need = v.unmapped_pages(ar, b);
+    if (need > v.spare_pages() && attempt == 2) {
+      v.reclaim(need);
+      c->n_reclaims++;
+    }
+    if (need <= v.spare_pages() && v.map_block(ar, b, &err)) {
+      void* prev = b->tag;
+      if (prev != kFresh && prev != stream) stream_wait_on(c, stream, prev);
+      b->tag = stream;
+      c->st.n_alloc++;
+      c->alloc_bytes += b->size;
+      c->alloc_peak = std::max(c->alloc_peak, c->alloc_bytes);
+      *out = ar.base() + b->off;
+      return LMS_OK;
+    }
+    v.pin(ar, b, -1);
+    ar.release(b);
   }
   c->st.n_oom++;
-  char buf[256];
+  char buf[320];
   snprintf(buf, sizeof buf,
-           "LMS_OOM: device budget exhausted allocating %zu bytes (in use %zu, limit %zu, "
-           "largest free block %zu)", size, c->dev.used(), c->limit, c->dev.largest_free());
+           "LMS_OOM: device budget exhausted allocating %zu bytes (live %zu, mapped %zu, limit %zu, "
+           "page %zu)%s%s", size, c->alloc_bytes, v.mapped_bytes(), c->limit, v.page(),
+           err.empty() ? "" : ": ", err.c_str());
   return fail(LMS_E_OOM, buf);
 }
 
 int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
   if (!ptr) return LMS_OK;
-  if (!c->dev.owns(ptr)) return fail(LMS_E_INVALID, "lms_dev_free: pointer not from the device pool");
-  Block* b = c->dev.find_live(static_cast<char*>(ptr) - c->dev_base);
+  if (!c->vmm || !c->vmm->owns(ptr)) return fail(LMS_E_INVALID, "lms_dev_free: pointer not from the device pool");
+  Block* b = c->vmm->find_live(ptr);
   if (!b) return fail(LMS_E_INVALID, "lms_dev_free: not a live allocation");
   b->tag = stream;
   c->st.n_free++;
@@ -287,7 +313,7 @@ int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
     c->st.n_deferred_frees++;
     return LMS_OK;
   }
-  c->dev.release(b);
+  release_block(c, b);
   return LMS_OK;
 }
 
@@ -595,8 +621,8 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
   } else {
     c->h2d = c->d2h;
   }
-  if (cfg->device_reserve) {
-    int rc = ensure_arena(c);
+  if (cfg->device_reserve || cfg->device_limit) {
+    int rc = ensure_pool(c);
     if (rc) {
       delete c;
       return rc;
@@ -632,7 +658,7 @@ int lms_destroy(lms_ctx* c) {
     cudaFreeHost(ch.base);
     delete ch.arena;
   }
-  if (c->dev_base) cudaFree(c->dev_base);
+  delete c->vmm;
   if (c->zvc_scratch) cudaFree(c->zvc_scratch);
   if (c->h2d && c->h2d != c->d2h) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
@@ -655,15 +681,21 @@ int lms_set_home_stream(lms_ctx* c, void* s) {
 int lms_set_limit(lms_ctx* c, size_t limit) {
   if (!c) return fail(LMS_E_INVALID, "null ctx");
   std::lock_guard<std::mutex> g(c->mu);
-  c->limit = limit;
+  if (limit == 0) limit = c->cfg.device_reserve ? c->cfg.device_reserve : c->limit;
   c->cfg.device_limit = limit;
-  if (c->dev_base && (limit == 0 || limit > c->dev.capacity())) c->limit = c->dev.capacity();
+  if (c->vmm) {
+    c->vmm->set_limit(limit);
+    c->limit = c->vmm->limit_bytes();
+  } else {
+    c->limit = limit;
+  }
   return LMS_OK;
 }
 
 int lms_reset_peaks(lms_ctx* c) {
   std::lock_guard<std::mutex> g(c->mu);
-  c->dev.reset_peak();
+  c->alloc_peak = c->alloc_bytes;
+  if (c->vmm) c->vmm->reset_mapped_peak();
   c->host_peak = c->host_used;
   return LMS_OK;
 }
@@ -690,8 +722,8 @@ int lms_dev_free(lms_ctx* c, void* ptr, void* stream) {
 int lms_dev_hold_until(lms_ctx* c, const void* ptr, void* stream) {
   if (!c || !ptr) return fail(LMS_E_INVALID, "null argument");
   std::lock_guard<std::mutex> g(c->mu);
-  if (!c->dev.owns(ptr)) return LMS_OK;  // not ours (e.g. default allocator): nothing to hold
-  Block* b = c->dev.containing(static_cast<const char*>(ptr) - c->dev_base);
+  if (!c->vmm || !c->vmm->owns(ptr)) return LMS_OK;  // not ours: nothing to hold
+  Block* b = c->vmm->containing(ptr);
   if (!b) return fail(LMS_E_INVALID, "lms_dev_hold_until: pointer not in a live block");
   auto* ev = new SharedEv();
   ev->e = c->events.get();
@@ -782,8 +814,8 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
     c->zvc_open.push_back(h);
   }
   // hold the source block until the copy is done
-  if (stored && c->dev_base && c->dev.owns(src)) {
-    Block* b = c->dev.containing(static_cast<const char*>(src) - c->dev_base);
+  if (stored && c->vmm && c->vmm->owns(src)) {
+    Block* b = c->vmm->containing(src);
     if (b) {
       h->out_done->refs++;
       c->holds[b].push_back(h->out_done);
@@ -984,11 +1016,16 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   reap_deferred(c, false);
   account_zvc(c);
   lms_stats_t s = c->st;
-  s.device_in_use = c->dev.used();
-  s.device_peak = c->dev.peak();
-  s.device_reserved = c->dev.capacity();
+  s.device_in_use = c->alloc_bytes;
+  s.device_peak = c->alloc_peak;
+  s.device_reserved = c->vmm ? c->vmm->va_bytes() : 0;
   s.device_limit = c->limit;
-  s.device_largest_free = c->dev.largest_free();
+  s.device_largest_free = c->vmm ? c->vmm->large_.largest_free() : 0;
+  s.device_mapped = c->vmm ? c->vmm->mapped_bytes() : 0;
+  s.device_mapped_peak = c->vmm ? c->vmm->mapped_peak_bytes() : 0;
+  s.n_map = c->vmm ? c->vmm->n_map() : 0;
+  s.n_unmap = c->vmm ? c->vmm->n_unmap() : 0;
+  s.n_reclaims = c->n_reclaims;
   s.device_deferred_bytes = c->deferred_bytes;
   s.host_in_use = c->host_used;
   s.host_peak = c->host_peak;

@@ -15,6 +15,7 @@ from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblms.so")
+SHIM_PATH = os.path.join(_HERE, "liblms_torch.so")   # PyTorch allocator hooks (throw c10 OOM)
 
 LMS_OK, LMS_E_INVALID, LMS_E_OOM, LMS_E_HOST_OOM, LMS_E_CUDA, LMS_E_STATE = 0, -1, -2, -3, -4, -5
 CODEC_RAW_CE, CODEC_RAW_SM, CODEC_ZVC = 0, 1, 2
@@ -39,7 +40,8 @@ class _Config(ctypes.Structure):
 
 _STAT_FIELDS = [
     "device_in_use", "device_peak", "device_reserved", "device_limit", "device_largest_free",
-    "device_deferred_bytes", "host_in_use", "host_peak", "host_reserved", "n_alloc", "n_free",
+    "device_deferred_bytes", "device_mapped", "device_mapped_peak", "n_map", "n_unmap", "n_reclaims",
+    "host_in_use", "host_peak", "host_reserved", "n_alloc", "n_free",
     "n_oom", "n_deferred_frees", "n_cross_stream_waits", "n_swap_out", "n_swap_in",
     "n_handles_live", "d2h_logical_bytes", "d2h_wire_bytes", "h2d_logical_bytes",
     "h2d_wire_bytes", "kernel_launches",
@@ -311,7 +313,9 @@ def install_allocator(ctx: Context):
     if _installed is not None:
         raise RuntimeError("a different LMS context already owns the PyTorch allocator")
     ctx.make_global()
-    alloc = torch.cuda.memory.CUDAPluggableAllocator(LIB_PATH, "lms_alloc", "lms_free")
+    if not os.path.exists(SHIM_PATH):
+        raise LmsError(f"{SHIM_PATH} is missing; run __graft_entry__.build()")
+    alloc = torch.cuda.memory.CUDAPluggableAllocator(SHIM_PATH, "lms_torch_alloc", "lms_torch_free")
     torch.cuda.memory.change_current_allocator(alloc)
     _installed = ctx
 

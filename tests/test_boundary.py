@@ -45,6 +45,14 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in lib.lms_version()
 
 
+def test_torch_shim_exports_allocator_hooks():
+    shim = os.path.join(ROOT, "paper_1807_02037_b200", "liblms_torch.so")
+    ctypes.CDLL(LIB, mode=ctypes.RTLD_GLOBAL)
+    import torch  # noqa: F401  (libc10 must be loadable)
+    lib = ctypes.CDLL(shim)
+    assert hasattr(lib, "lms_torch_alloc") and hasattr(lib, "lms_torch_free")
+
+
 def test_cubin_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout

@@ -56,18 +56,33 @@ def test_ffchain_swap_equals_noswap_and_oracle(lms_ctx, L, N):
             assert _rel(base[k], ref[k]) < 1e-5, k
 
 
-def test_swapping_lowers_peak_when_compute_hides_copies(lms_ctx):
-    """N=4096: each matmul (~2.7 ms fp32) outlasts a 64 MiB D2H, so swap-outs
-    finish in time and the pool's high-water mark drops (the simulator's
-    criterion-5 effect, measured)."""
-    L, N = 8, 4096
+def test_swapping_fits_a_budget_no_swap_cannot(lms_ctx):
+    """Criterion-5 effect on hardware: under a pool limit below the no-swap
+    working set, the plain schedule runs out of memory and the rewritten one
+    completes with bit-identical results (the pool waits for pending D2H
+    copies before refusing an allocation)."""
+    L, N = 8, 2048
+    tb = N * N * 4
     g = ffchain(L, N)
     inputs = ffchain_inputs(g, N, seed=1)
-    _, rep0 = execute(g, inputs, ExecConfig(), ctx=lms_ctx)
+    base, rep0 = execute(g, inputs, ExecConfig(), ctx=lms_ctx)
     g2, _ = rewrite(g, RewriteConfig(lb=1, ub=3))
-    _, rep = execute(g2, inputs, ExecConfig(codec="ce"), ctx=lms_ctx)
-    assert rep.peak_device_bytes < rep0.peak_device_bytes
-    assert rep.peak_host_bytes >= L * N * N * 4
+    torch.cuda.synchronize()
+    lms_ctx.synchronize()
+    in_use = lms_ctx.stats()["device_in_use"]
+    staged = (L + 1) * tb                       # inputs bound by execute()
+    limit = in_use + staged + rep0.peak_device_bytes - 3 * tb
+    lms_ctx.set_limit(limit)
+    try:
+        with pytest.raises(RuntimeError, match="LMS_OOM"):
+            execute(g, inputs, ExecConfig(), ctx=lms_ctx)
+        torch.cuda.synchronize()
+        got, rep = execute(g2, inputs, ExecConfig(codec="ce"), ctx=lms_ctx)
+    finally:
+        lms_ctx.set_limit(0)
+    for k in base:
+        assert np.array_equal(got[k], base[k]), k
+    assert rep.peak_host_bytes >= L * tb
 
 
 def test_report_schema(lms_ctx):
