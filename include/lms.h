@@ -75,7 +75,7 @@ typedef struct {
   uint64_t device_reserved, device_limit;      /* VA reserved; physical budget */
   uint64_t device_largest_free, device_deferred_bytes;
   uint64_t device_mapped, device_mapped_peak;  /* physical pages actually backing blocks */
-  uint64_t n_map, n_unmap, n_reclaims;
+  uint64_t n_map, n_unmap, n_reclaims, n_device_syncs;
   uint64_t host_in_use, host_peak, host_reserved;
   uint64_t n_alloc, n_free, n_oom, n_deferred_frees, n_cross_stream_waits;
   uint64_t n_swap_out, n_swap_in, n_handles_live;
@@ -84,6 +84,7 @@ typedef struct {
   uint64_t kernel_launches;                     /* our sm_100a kernels */
   double d2h_busy_ms, h2d_busy_ms;              /* sum of transfer spans (timing=1) */
   double swap_wait_ms;  /* consumer stalls on swap-ins (timing=1): transfer_wait_total */
+  double pool_driver_ms;   /* host time in cuMemMap / cuMemSetAccess / cuMemUnmap */
 } lms_stats_t;
 
 /* one measured transfer, in the TraceEvent vocabulary (sim.py:74-81) */

@@ -8,6 +8,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <iterator>
 #include <map>
 #include <set>
 #include <utility>
@@ -71,6 +72,12 @@ class Arena {
       if (it == free_.end()) return nullptr;
       pick = it->second;
     }
+    return take(it, size);
+  }
+
+  template <class It>
+  Block* take(It it, size_t size) {
+    Block* pick = it->second;
     free_.erase(it);
     if (pick->size - size >= align_) {
       Block* rest = new Block();
@@ -147,6 +154,27 @@ class Arena {
 
   bool mergeable(const Block* a, const Block* b) const {
     return a->tag == b->tag || a->tag == fresh_ || b->tag == fresh_;
+  }
+
+  // Best fit guided by a cost: among the first `scan` free blocks of adequate
+  // size (ascending size), take the lowest cost(block, size); ties keep the
+  // smaller block.  Lets the device pool prefer ranges whose pages are mapped.
+  template <class Cost>
+  Block* alloc_scored(size_t size, Cost cost, int scan = 48) {
+    size = round_up(size);
+    auto it = free_.lower_bound({size, nullptr});
+    if (it == free_.end()) return nullptr;
+    auto best = it;
+    long best_cost = cost(it->second, size);
+    int n = 1;
+    for (auto jt = std::next(it); jt != free_.end() && n < scan && best_cost > 0; ++jt, ++n) {
+      long c = cost(jt->second, size);
+      if (c < best_cost) {
+        best_cost = c;
+        best = jt;
+      }
+    }
+    return take(best, size);
   }
 
   // Live block containing the byte at `off`, or nullptr.

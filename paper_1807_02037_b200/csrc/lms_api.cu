@@ -135,7 +135,7 @@ struct lms_ctx {
   VmmPool* vmm = nullptr;
   size_t limit = 0;
   size_t alloc_bytes = 0, alloc_peak = 0;   // live block bytes (the model's residency)
-  uint64_t n_reclaims = 0;
+  uint64_t n_reclaims = 0, n_device_syncs = 0;
   std::unordered_map<Block*, std::vector<SharedEv*>> holds;
   std::vector<Block*> deferred;
   size_t deferred_bytes = 0;
@@ -266,11 +266,15 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
     }
     if (attempt == 2) {
       cudaDeviceSynchronize();
+      c->n_device_syncs++;
       reap_deferred(c, true);
       v.small_.retag_all_free(kFresh);
       v.large_.retag_all_free(kFresh);
     }
-    Block* b = ar.alloc(size, stream);
+    // prefer ranges whose pages are already mapped, then the caller's stream
+    Block* b = ar.alloc_scored(size, [&](const Block* fb, size_t sz) -> long {
+      return 4 * v.unmapped_prefix(ar, fb, sz) + (fb->tag != stream && fb->tag != kFresh ? 1 : 0);
+    });
     if (!b) continue;
     v.pin(ar, b, +1);
     size_t need = v.unmapped_pages(ar, b);
@@ -1026,6 +1030,8 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   s.n_map = c->vmm ? c->vmm->n_map() : 0;
   s.n_unmap = c->vmm ? c->vmm->n_unmap() : 0;
   s.n_reclaims = c->n_reclaims;
+  s.n_device_syncs = c->n_device_syncs;
+  s.pool_driver_ms = c->vmm ? c->vmm->driver_ms() : 0;
   s.device_deferred_bytes = c->deferred_bytes;
   s.host_in_use = c->host_used;
   s.host_peak = c->host_peak;

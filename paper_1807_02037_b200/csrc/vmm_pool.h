@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -136,7 +137,18 @@ class VmmPool {
     return n;
   }
 
-  size_t spare_pages() const { return free_handles_.size() + (limit_pages_ - std::min(limit_pages_, created_)); }
+  // pages that may still be mapped under the budget
+  size_t spare_pages() const { return mapped_ >= limit_pages_ ? 0 : limit_pages_ - mapped_; }
+
+  // unmapped pages in the first `size` bytes of free block b (the part an
+  // allocation of `size` would use)
+  long unmapped_prefix(const Arena& a, const Block* b, size_t size) const {
+    size_t lo = size_t(a.base() - base_) + b->off;
+    size_t f = lo / page_, l = (lo + size - 1) / page_;
+    long n = 0;
+    for (size_t p = f; p <= l; ++p) n += handle_of_[p] < 0;
+    return n;
+  }
 
   void pin(Arena& a, const Block* b, int delta) {
     size_t f, l;
@@ -145,10 +157,14 @@ class VmmPool {
   }
 
   // unmap pages no live block touches until `want` spare pages exist;
-  // the caller has made sure no in-flight work uses free ranges
+  // the caller has made sure no in-flight work uses free ranges.  Pages are
+  // taken from the top of the address space down (the large arena grows
+  // upward from fresh VA, so the highest cached pages are the coldest).
   size_t reclaim(size_t want) {
+    auto t0 = std::chrono::steady_clock::now();
     size_t got = 0;
-    for (size_t p = 0; p < handle_of_.size() && spare_pages() < want; ++p) {
+    for (size_t q = handle_of_.size(); q-- > 0 && spare_pages() < want;) {
+      size_t p = q;
       if (handle_of_[p] >= 0 && live_[p] == 0) {
         drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
         free_handles_.push_back(handle_of_[p]);
@@ -165,6 +181,7 @@ class VmmPool {
       free_handles_.pop_back();
       --created_;
     }
+    driver_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return got;
   }
 
@@ -172,6 +189,13 @@ class VmmPool {
   bool map_block(Arena& a, const Block* b, std::string* err) {
     size_t f, l;
     page_span(a, b, &f, &l);
+    if (unmapped_pages(a, b) == 0) return true;
+    auto t0 = std::chrono::steady_clock::now();
+    struct Acc {
+      double* s;
+      std::chrono::steady_clock::time_point t0;
+      ~Acc() { *s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+    } acc{&driver_s_, t0};
     size_t run = SIZE_MAX;
     for (size_t p = f; p <= l + 1; ++p) {
       bool need = p <= l && handle_of_[p] < 0;
@@ -206,6 +230,7 @@ class VmmPool {
   size_t mapped_peak_bytes() const { return mapped_peak_ * page_; }
   void reset_mapped_peak() { mapped_peak_ = mapped_; }
   uint64_t n_map() const { return n_map_; }
+  double driver_ms() const { return driver_s_ * 1e3; }
   uint64_t n_unmap() const { return n_unmap_; }
   size_t va_bytes() const { return small_va_ + large_va_; }
 
@@ -213,14 +238,14 @@ class VmmPool {
 
  private:
   int take_handle(std::string* err) {
+    if (mapped_ >= limit_pages_) {
+      *err = "physical page budget exhausted";
+      return -1;
+    }
     if (!free_handles_.empty()) {
       int h = free_handles_.back();
       free_handles_.pop_back();
       return h;
-    }
-    if (created_ >= limit_pages_) {
-      *err = "physical page budget exhausted";
-      return -1;
     }
     CUmemGenericAllocationHandle hd = 0;
     if (drv_.create(&hd, page_, &prop_, 0) != CUDA_SUCCESS) {
@@ -263,6 +288,7 @@ class VmmPool {
   std::vector<int> free_handles_;       // created, currently unmapped
   size_t created_ = 0, limit_pages_ = 0, mapped_ = 0, mapped_peak_ = 0;
   uint64_t n_map_ = 0, n_unmap_ = 0;
+  double driver_s_ = 0;
 };
 
 }  // namespace lms

@@ -40,7 +40,7 @@ class _Config(ctypes.Structure):
 
 _STAT_FIELDS = [
     "device_in_use", "device_peak", "device_reserved", "device_limit", "device_largest_free",
-    "device_deferred_bytes", "device_mapped", "device_mapped_peak", "n_map", "n_unmap", "n_reclaims",
+    "device_deferred_bytes", "device_mapped", "device_mapped_peak", "n_map", "n_unmap", "n_reclaims", "n_device_syncs",
     "host_in_use", "host_peak", "host_reserved", "n_alloc", "n_free",
     "n_oom", "n_deferred_frees", "n_cross_stream_waits", "n_swap_out", "n_swap_in",
     "n_handles_live", "d2h_logical_bytes", "d2h_wire_bytes", "h2d_logical_bytes",
@@ -51,7 +51,7 @@ _STAT_FIELDS = [
 class _Stats(ctypes.Structure):
     _fields_ = [(f, ctypes.c_uint64) for f in _STAT_FIELDS] + [
         ("d2h_busy_ms", ctypes.c_double), ("h2d_busy_ms", ctypes.c_double),
-        ("swap_wait_ms", ctypes.c_double)]
+        ("swap_wait_ms", ctypes.c_double), ("pool_driver_ms", ctypes.c_double)]
 
 
 class _Xfer(ctypes.Structure):
