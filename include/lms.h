@@ -165,6 +165,8 @@ int lms_zvc_decode(lms_ctx* ctx, const void* enc, size_t nwords, void* dst, void
 int lms_zvc_encoded_size(const void* enc_host, size_t* out);
 
 /* ---- stats / trace -------------------------------------------------------- */
+/* sizes of live device blocks, largest first (diagnostics); *n = total count */
+int lms_live_blocks(lms_ctx* ctx, uint64_t* sizes, size_t cap, size_t* n);
 int lms_stats(lms_ctx* ctx, lms_stats_t* out);
 /* copies up to `cap` finished transfer records; returns count via *n */
 int lms_trace(lms_ctx* ctx, lms_xfer_record_t* out, size_t cap, size_t* n);

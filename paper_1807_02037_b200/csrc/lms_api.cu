@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -296,6 +297,16 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
     ar.release(b);
   }
   c->st.n_oom++;
+  if (getenv("LMS_DEBUG_OOM")) {
+    std::vector<uint64_t> sz;
+    v.small_.for_each_live([&](Block* b) { sz.push_back(b->size); });
+    v.large_.for_each_live([&](Block* b) { sz.push_back(b->size); });
+    std::sort(sz.begin(), sz.end(), std::greater<uint64_t>());
+    fprintf(stderr, "[lms] OOM wanting %zu B: %zu live blocks, deferred %zu B, largest:", size, sz.size(),
+            c->deferred_bytes);
+    for (size_t i = 0; i < sz.size() && i < 16; ++i) fprintf(stderr, " %.0fM", sz[i] / 1048576.0);
+    fprintf(stderr, "\n");
+  }
   char buf[320];
   snprintf(buf, sizeof buf,
            "LMS_OOM: device budget exhausted allocating %zu bytes (live %zu, mapped %zu, limit %zu, "
@@ -1055,6 +1066,22 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   }
   s.swap_wait_ms = stall;
   *out = s;
+  return LMS_OK;
+}
+
+int lms_live_blocks(lms_ctx* c, uint64_t* sizes, size_t cap, size_t* n) {
+  if (!c || !n) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  std::vector<uint64_t> v;
+  if (c->vmm) {
+    c->vmm->small_.for_each_live([&](Block* b) { v.push_back(b->size); });
+    c->vmm->large_.for_each_live([&](Block* b) { v.push_back(b->size); });
+  }
+  std::sort(v.begin(), v.end(), std::greater<uint64_t>());
+  size_t k = std::min(cap, v.size());
+  if (sizes)
+    for (size_t i = 0; i < k; ++i) sizes[i] = v[i];
+  *n = v.size();
   return LMS_OK;
 }
 

@@ -98,6 +98,7 @@ def lib():
         "lms_stats": ([vp, ctypes.POINTER(_Stats)], i),
         "lms_trace": ([vp, ctypes.POINTER(_Xfer), sz, ctypes.POINTER(sz)], i),
         "lms_trace_clear": ([vp], i), "lms_synchronize": ([vp], i),
+        "lms_live_blocks": ([vp, ctypes.POINTER(ctypes.c_uint64), sz, ctypes.POINTER(sz)], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -292,6 +293,13 @@ class Context:
         n = ctypes.c_size_t()
         _check(lib().lms_trace(self.ptr, buf, cap, ctypes.byref(n)), "lms_trace")
         return [{f: getattr(buf[k], f) for f, _ in _Xfer._fields_} for k in range(n.value)]
+
+    def live_blocks(self, cap: int = 64) -> tuple[int, list[int]]:
+        """(number of live device blocks, sizes of the largest ``cap``)."""
+        buf = (ctypes.c_uint64 * cap)()
+        n = ctypes.c_size_t()
+        _check(lib().lms_live_blocks(self.ptr, buf, cap, ctypes.byref(n)), "lms_live_blocks")
+        return n.value, [buf[i] for i in range(min(cap, n.value))]
 
     def trace_clear(self):
         _check(lib().lms_trace_clear(self.ptr), "lms_trace_clear")

@@ -168,12 +168,18 @@ class _Capture:
         return t
 
 
-def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16):
+def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
     """Trace one step — ``forward_fn()`` returns the loss, backward runs here — into a CompGraph.
 
-    Returns (graph, meta) where meta maps graph ids back to pack indices and
-    autograd-node ranks.  The traced step's gradients are left in place.
+    ``persistent``: tensors that outlive the step (parameters, buffers, the
+    step's inputs); saved references to them become variable reads and are
+    never swapped.  Any other saved tensor without a ``grad_fn`` (pooling
+    indices, saved batch statistics, workspaces) is an output of the op that
+    saves it.  Returns (graph, meta) where meta maps graph ids back to pack
+    indices and autograd-node ranks.  The traced step's gradients are left in
+    place.
     """
+    keep_ptrs = {t.data_ptr() for t in persistent if t is not None and t.numel()}
     cap = _Capture()
     with torch.autograd.graph.saved_tensors_hooks(cap.pack, cap.unpack):
         loss = forward_fn()
@@ -239,14 +245,12 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16):
             continue
         s = by_key.get(key)
         if s is None:
-            if is_param or (is_leaf and req):
-                producer = None
+            if is_param or (is_leaf and req) or key[0] in keep_ptrs:
+                producer = None   # parameter, buffer or step input: a variable
             elif grad_fn is not None and grad_fn in rank:
                 producer = grad_fn
-            elif is_leaf:
-                producer = None  # a step input
             else:
-                producer = "self"
+                producer = "self"  # non-differentiable output of the saving op
             s = _Saved(len(saved), nbytes, producer, is_param)
             by_key[key] = s
             saved.append(s)
@@ -514,7 +518,9 @@ class LMS:
     def capture(self, x, y):
         """Trace one step at (x, y) — no optimizer update — and build the swap plan."""
         self.optimizer.zero_grad(set_to_none=True)
-        self.graph, self.meta = capture_graph(lambda: self.loss_fn(self.model(x), y), self.min_swap_bytes)
+        persistent = list(self.model.parameters()) + list(self.model.buffers()) + [x, y]
+        self.graph, self.meta = capture_graph(lambda: self.loss_fn(self.model(x), y), self.min_swap_bytes,
+                                              persistent)
         self.optimizer.zero_grad(set_to_none=True)
         self.replan(self.cfg)
         return self.plan
