@@ -245,6 +245,10 @@ int ensure_pool(lms_ctx* c) {
     delete v;
     return fail(LMS_E_CUDA, "device pool: " + err);
   }
+  if (c->cfg.device_reserve && !v->precreate(c->cfg.device_reserve / v->page(), &err)) {
+    delete v;
+    return fail(LMS_E_CUDA, "device pool: " + err);
+  }
   c->vmm = v;
   c->limit = v->limit_bytes();
   return LMS_OK;
@@ -260,7 +264,14 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
   Arena& ar = v.arena_for(size);
   reap_deferred(c, false);
   std::string err;
-  for (int attempt = 0; attempt < 3; ++attempt) {
+  // live bytes can never shrink below the non-deferred live set: if that plus
+  // the request exceeds the budget, fail now instead of draining the device
+  // and flushing the page cache (cuDNN's plan loop probes oversized
+  // workspaces and expects a quick OOM)
+  const size_t want_pages = (size + v.page() - 1) / v.page();
+  const size_t live_pages = (c->alloc_bytes - c->deferred_bytes + v.page() - 1) / v.page();
+  bool hopeless = size > VmmPool::kSmallMax && live_pages + want_pages > c->limit / v.page();
+  for (int attempt = 0; attempt < 3 && !(hopeless && attempt > 0); ++attempt) {
     if (attempt == 1) {
       if (c->deferred.empty()) continue;
       reap_deferred(c, true);

@@ -176,8 +176,10 @@ class VmmPool {
     }
     // over the (possibly lowered) limit: drop surplus physical pages
     while (created_ > limit_pages_ && !free_handles_.empty()) {
-      drv_.release(handles_[free_handles_.back()]);
-      handles_[free_handles_.back()] = 0;
+      int h = free_handles_.back();
+      drv_.release(handles_[h]);
+      handles_[h] = 0;
+      free_slots_.push_back(h);
       free_handles_.pop_back();
       --created_;
     }
@@ -227,6 +229,7 @@ class VmmPool {
   }
 
   size_t mapped_bytes() const { return mapped_ * page_; }
+  size_t created_pages() const { return created_; }
   size_t mapped_peak_bytes() const { return mapped_peak_ * page_; }
   void reset_mapped_peak() { mapped_peak_ = mapped_; }
   uint64_t n_map() const { return n_map_; }
@@ -252,18 +255,39 @@ class VmmPool {
       *err = "cuMemCreate failed (device out of physical memory?)";
       return -1;
     }
-    int idx = -1;
-    for (size_t i = 0; i < handles_.size(); ++i)
-      if (handles_[i] == 0) { idx = int(i); break; }
-    if (idx < 0) {
+    int idx;
+    if (!free_slots_.empty()) {
+      idx = free_slots_.back();
+      free_slots_.pop_back();
+      handles_[idx] = hd;
+    } else {
       idx = int(handles_.size());
       handles_.push_back(hd);
-    } else {
-      handles_[idx] = hd;
     }
     ++created_;
     return idx;
   }
+
+ public:
+  // create physical pages up front (cuMemCreate is the slow driver call) so
+  // that steady-state remaps only pay cuMemMap/cuMemSetAccess
+  bool precreate(size_t pages, std::string* err) {
+    auto t0 = std::chrono::steady_clock::now();
+    while (created_ < std::min(pages, limit_pages_)) {
+      CUmemGenericAllocationHandle hd = 0;
+      if (drv_.create(&hd, page_, &prop_, 0) != CUDA_SUCCESS) {
+        *err = "cuMemCreate failed while pre-creating pages";
+        return false;
+      }
+      handles_.push_back(hd);
+      free_handles_.push_back(int(handles_.size()) - 1);
+      ++created_;
+    }
+    driver_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return true;
+  }
+
+ private:
 
   void teardown() {
     if (!base_) return;
@@ -286,6 +310,7 @@ class VmmPool {
   std::vector<uint16_t> live_;          // page -> live blocks touching it
   std::vector<CUmemGenericAllocationHandle> handles_;
   std::vector<int> free_handles_;       // created, currently unmapped
+  std::vector<int> free_slots_;         // released slots in handles_
   size_t created_ = 0, limit_pages_ = 0, mapped_ = 0, mapped_peak_ = 0;
   uint64_t n_map_ = 0, n_unmap_ = 0;
   double driver_s_ = 0;
