@@ -29,6 +29,7 @@ import os
 import subprocess
 import sys
 import time
+import traceback
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -215,6 +216,7 @@ def main():
             if not is_oom(e):
                 raise
             ok = False
+            traceback.clear_frames(e.__traceback__)
         x = y = None
         opt.zero_grad(set_to_none=True)
         gc.collect()
@@ -332,6 +334,7 @@ def main():
                 raise
             ok = False
             log(f"[bench] OOM at batch {nb} n_tensors={n_tensors}: {str(e)[:160]}")
+            traceback.clear_frames(e.__traceback__)
         xb = yb = None
         attempts.append({"batch": nb, "n_tensors": n_tensors, "ok": ok})
         ok = agree(1.0 if ok else 0.0) > 0.5

@@ -469,29 +469,40 @@ class SwapExecutor:
                 group_tensor.pop(gid, None)  # the consumer node holds it until it finishes
             return t
 
-        with torch.autograd.graph.saved_tensors_hooks(pack, unpack):
-            loss = forward_fn()
-        if k_counter[0] != plan.n_packs:
-            raise RuntimeError(f"step saved {k_counter[0]} tensors but the plan was captured with "
-                               f"{plan.n_packs}; re-capture the plan for this model/step")
-        # hook the control ops of this step's graph
         hooks = []
-        if plan.triggers:
-            ops = sorted((n for n in _walk(loss.grad_fn) if not _is_accumulate(n)),
-                         key=lambda n: n._sequence_nr())
-            seq0 = ops[0]._sequence_nr()
-            for n in ops:
-                gids = plan.triggers.get(n._sequence_nr() - seq0)
-                if gids:
-                    hooks.append(n.register_hook(_issuer(issue, gids)))
-        for gid in plan.bwd_start_groups:
-            issue(gid)
-        loss.backward()
-        for h in hooks:
-            h.remove()
-        for h in handles.values():
-            ctx.release(h)
-        group_tensor.clear()
+        loss = None
+        try:
+            with torch.autograd.graph.saved_tensors_hooks(pack, unpack):
+                loss = forward_fn()
+            if k_counter[0] != plan.n_packs:
+                raise RuntimeError(f"step saved {k_counter[0]} tensors but the plan was captured with "
+                                   f"{plan.n_packs}; re-capture the plan for this model/step")
+            # hook the control ops of this step's graph
+            if plan.triggers:
+                ops = sorted((n for n in _walk(loss.grad_fn) if not _is_accumulate(n)),
+                             key=lambda n: n._sequence_nr())
+                seq0 = ops[0]._sequence_nr()
+                for n in ops:
+                    gids = plan.triggers.get(n._sequence_nr() - seq0)
+                    if gids:
+                        hooks.append(n.register_hook(_issuer(issue, gids)))
+            for gid in plan.bwd_start_groups:
+                issue(gid)
+            loss.backward()
+        except BaseException:
+            # a failed step (e.g. the budget is too small) must not pin the
+            # graph, the swapped-in tensors or the host copies: the exception's
+            # traceback keeps this frame alive
+            loss = None
+            raise
+        finally:
+            for hk in hooks:
+                hk.remove()
+            hooks.clear()
+            group_tensor.clear()
+            for h in handles.values():
+                ctx.release(h)
+            handles.clear()
         return loss
 
 
