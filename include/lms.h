@@ -73,7 +73,7 @@ typedef struct {
 typedef struct {
   uint64_t device_in_use, device_peak;         /* live block bytes (the model's residency) */
   uint64_t device_reserved, device_limit;      /* VA reserved; physical budget */
-  uint64_t device_largest_free, device_deferred_bytes;
+  uint64_t device_cached, device_deferred_bytes;   /* mapped free blocks; frees awaiting swap-outs */
   uint64_t device_mapped, device_mapped_peak;  /* physical pages actually backing blocks */
   uint64_t n_map, n_unmap, n_reclaims, n_device_syncs;
   uint64_t host_in_use, host_peak, host_reserved;

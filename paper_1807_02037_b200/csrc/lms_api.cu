@@ -97,6 +97,16 @@ struct XferRec {
   cudaEvent_t start, end;
 };
 
+// a live device allocation: small (arena block) or large (mapped VA range)
+struct DevBlk {
+  char* base = nullptr;
+  size_t size = 0;
+  Block* small = nullptr;
+  Big* big = nullptr;
+  void* stream = nullptr;          // freeing stream (deferred blocks)
+  cudaEvent_t free_ev = nullptr;   // recorded at free on that stream (large blocks)
+};
+
 }  // namespace lms
 
 using namespace lms;
@@ -137,8 +147,9 @@ struct lms_ctx {
   size_t limit = 0;
   size_t alloc_bytes = 0, alloc_peak = 0;   // live block bytes (the model's residency)
   uint64_t n_reclaims = 0, n_device_syncs = 0;
-  std::unordered_map<Block*, std::vector<SharedEv*>> holds;
-  std::vector<Block*> deferred;
+  size_t mapped_peak = 0;
+  std::unordered_map<char*, std::vector<SharedEv*>> holds;  // block base -> pending readers
+  std::vector<DevBlk> deferred;                             // freed, waiting for their holds
   size_t deferred_bytes = 0;
 
   // pinned host pool: chunks, each an arena
@@ -180,8 +191,8 @@ void retire_event(lms_ctx* c, SharedEv* ev) {
 }
 
 // drop completed holds; true if the block has none left
-bool holds_clear(lms_ctx* c, Block* b) {
-  auto it = c->holds.find(b);
+bool holds_clear(lms_ctx* c, char* base) {
+  auto it = c->holds.find(base);
   if (it == c->holds.end()) return true;
   auto& v = it->second;
   size_t w = 0;
@@ -197,27 +208,36 @@ bool holds_clear(lms_ctx* c, Block* b) {
   return false;
 }
 
-void release_block(lms_ctx* c, Block* b) {
-  Arena& ar = *b->owner;
-  c->vmm->pin(ar, b, -1);
-  c->alloc_bytes -= b->size;
-  ar.release(b);
+void drain_pool_events(lms_ctx* c) {
+  for (auto e : c->vmm->events_done_) c->events.put(e);
+  c->vmm->events_done_.clear();
+}
+
+// give a freed block back to the pool (large blocks go to the mapped cache)
+void release_block(lms_ctx* c, const DevBlk& d) {
+  c->alloc_bytes -= d.size;
+  if (d.small) {
+    d.small->tag = d.stream;
+    c->vmm->small_free(d.small);
+  } else {
+    c->vmm->big_free(d.big, d.stream, d.free_ev);
+  }
 }
 
 void reap_deferred(lms_ctx* c, bool block) {
   size_t w = 0;
   for (size_t i = 0; i < c->deferred.size(); ++i) {
-    Block* b = c->deferred[i];
+    DevBlk& d = c->deferred[i];
     if (block) {
-      auto it = c->holds.find(b);
+      auto it = c->holds.find(d.base);
       if (it != c->holds.end())
         for (auto* ev : it->second) cudaEventSynchronize(ev->e);
     }
-    if (holds_clear(c, b)) {
-      c->deferred_bytes -= b->size;
-      release_block(c, b);
+    if (holds_clear(c, d.base)) {
+      c->deferred_bytes -= d.size;
+      release_block(c, d);
     } else {
-      c->deferred[w++] = b;
+      c->deferred[w++] = d;
     }
   }
   c->deferred.resize(w);
@@ -254,92 +274,135 @@ int ensure_pool(lms_ctx* c) {
   return LMS_OK;
 }
 
-// returns LMS_OK and *out, or LMS_E_OOM.  Escalation when the budget is
-// short: (0) as is, (1) wait for deferred frees (pending swap-out copies),
-// (2) drain the device, merge stream-split ranges and unmap idle cached pages.
-int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
-  int rc = ensure_pool(c);
-  if (rc) return rc;
+void note_alloc(lms_ctx* c, size_t bytes) {
+  c->st.n_alloc++;
+  c->alloc_bytes += bytes;
+  c->alloc_peak = std::max(c->alloc_peak, c->alloc_bytes);
+  c->mapped_peak = std::max(c->mapped_peak, c->vmm->mapped_bytes());
+}
+
+int oom(lms_ctx* c, size_t size, const std::string& why) {
   VmmPool& v = *c->vmm;
-  Arena& ar = v.arena_for(size);
-  reap_deferred(c, false);
-  std::string err;
-  // live bytes can never shrink below the non-deferred live set: if that plus
-  // the request exceeds the budget, fail now instead of draining the device
-  // and flushing the page cache (cuDNN's plan loop probes oversized
-  // workspaces and expects a quick OOM)
-  const size_t want_pages = (size + v.page() - 1) / v.page();
-  const size_t live_pages = (c->alloc_bytes - c->deferred_bytes + v.page() - 1) / v.page();
-  bool hopeless = size > VmmPool::kSmallMax && live_pages + want_pages > c->limit / v.page();
-  for (int attempt = 0; attempt < 3 && !(hopeless && attempt > 0); ++attempt) {
-    if (attempt == 1) {
-      if (c->deferred.empty()) continue;
-      reap_deferred(c, true);
-    }
-    if (attempt == 2) {
-      cudaDeviceSynchronize();
-      c->n_device_syncs++;
-      reap_deferred(c, true);
-      v.small_.retag_all_free(kFresh);
-      v.large_.retag_all_free(kFresh);
-    }
-    // prefer ranges whose pages are already mapped, then the caller's stream
-    Block* b = ar.alloc_scored(size, [&](const Block* fb, size_t sz) -> long {
-      return 4 * v.unmapped_prefix(ar, fb, sz) + (fb->tag != stream && fb->tag != kFresh ? 1 : 0);
-    });
-    if (!b) continue;
-    v.pin(ar, b, +1);
-    size_t need = v.unmapped_pages(ar, b);
-    if (need > v.spare_pages() && attempt == 2) {
-      v.reclaim(need);
-      c->n_reclaims++;
-    }
-    if (need <= v.spare_pages() && v.map_block(ar, b, &err)) {
-      void* prev = b->tag;
-      if (prev != kFresh && prev != stream) stream_wait_on(c, stream, prev);
-      b->tag = stream;
-      c->st.n_alloc++;
-      c->alloc_bytes += b->size;
-      c->alloc_peak = std::max(c->alloc_peak, c->alloc_bytes);
-      *out = ar.base() + b->off;
-      return LMS_OK;
-    }
-    v.pin(ar, b, -1);
-    ar.release(b);
-  }
   c->st.n_oom++;
   if (getenv("LMS_DEBUG_OOM")) {
     std::vector<uint64_t> sz;
-    v.small_.for_each_live([&](Block* b) { sz.push_back(b->size); });
-    v.large_.for_each_live([&](Block* b) { sz.push_back(b->size); });
+    v.for_each_live([&](uint64_t s) { sz.push_back(s); });
     std::sort(sz.begin(), sz.end(), std::greater<uint64_t>());
-    fprintf(stderr, "[lms] OOM wanting %zu B: %zu live blocks, deferred %zu B, largest:", size, sz.size(),
-            c->deferred_bytes);
+    fprintf(stderr, "[lms] OOM wanting %zu B: %zu live blocks, deferred %zu B, cached %zu B, largest:", size,
+            sz.size(), c->deferred_bytes, v.cached_bytes());
     for (size_t i = 0; i < sz.size() && i < 16; ++i) fprintf(stderr, " %.0fM", sz[i] / 1048576.0);
     fprintf(stderr, "\n");
   }
   char buf[320];
   snprintf(buf, sizeof buf,
            "LMS_OOM: device budget exhausted allocating %zu bytes (live %zu, mapped %zu, limit %zu, "
-           "page %zu)%s%s", size, c->alloc_bytes, v.mapped_bytes(), c->limit, v.page(),
-           err.empty() ? "" : ": ", err.c_str());
+           "page %zu): %s", size, c->alloc_bytes, v.mapped_bytes(), c->limit, v.page(), why.c_str());
   return fail(LMS_E_OOM, buf);
+}
+
+// returns LMS_OK and *out, or LMS_E_OOM.  Escalation when pages are short:
+// evict finished cached blocks, then wait for deferred frees (pending
+// swap-out copies), then wait for unfinished cached blocks.
+int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
+  int rc = ensure_pool(c);
+  if (rc) return rc;
+  VmmPool& v = *c->vmm;
+  reap_deferred(c, false);
+  std::string err;
+  const size_t rsize = Arena::round(size);
+  if (size <= VmmPool::kSmallMax) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      if (attempt == 1) reap_deferred(c, true);
+      if (attempt > 0) {
+        // a small block spans at most two pages: evict cache for them
+        v.make_room(2, attempt == 2);
+        drain_pool_events(c);
+      }
+      Block* b = v.small_alloc(size, stream, &err);
+      if (b) {
+        void* prev = b->tag;
+        if (prev != kFresh && prev != stream) stream_wait_on(c, stream, prev);
+        b->tag = stream;
+        note_alloc(c, b->size);
+        *out = v.small_ptr(b);
+        return LMS_OK;
+      }
+    }
+    drain_pool_events(c);
+    return oom(c, size, err);
+  }
+  const size_t pages = (rsize + v.page() - 1) / v.page();
+  bool needs_wait = false;
+  Big* b = v.big_from_cache(pages, stream, &needs_wait);
+  if (b) {
+    if (needs_wait) {
+      CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), b->ev, 0));
+      c->st.n_cross_stream_waits++;
+    }
+    if (b->ev) c->events.put(b->ev);
+    b->ev = nullptr;
+  } else {
+    // the non-deferred live set can only shrink by frees the caller has not
+    // made yet: if it plus this request exceeds the budget, fail now (cuDNN's
+    // plan loop probes oversized workspaces and expects a quick OOM)
+    const size_t live_pages = (c->alloc_bytes - c->deferred_bytes + v.page() - 1) / v.page();
+    if (live_pages + pages > c->limit / v.page()) {
+      drain_pool_events(c);
+      return oom(c, size, "live set plus request exceeds the budget");
+    }
+    b = v.big_fresh(rsize, pages, false, &err);
+    if (!b && !c->deferred.empty()) {
+      reap_deferred(c, true);
+      b = v.big_fresh(rsize, pages, false, &err);
+    }
+    if (!b) b = v.big_fresh(rsize, pages, true, &err);
+    drain_pool_events(c);
+    if (!b) return oom(c, size, err);
+  }
+  v.big_live(b, rsize);
+  note_alloc(c, rsize);
+  *out = v.ptr(b);
+  return LMS_OK;
+}
+
+bool find_dev(lms_ctx* c, const void* ptr, bool exact, DevBlk* d) {
+  VmmPool& v = *c->vmm;
+  if (v.is_small(ptr)) {
+    Block* b = exact ? v.small_find(ptr) : v.small_containing(ptr);
+    if (!b) return false;
+    d->base = v.small_ptr(b);
+    d->size = b->size;
+    d->small = b;
+    d->big = nullptr;
+    return true;
+  }
+  Big* b = exact ? v.big_find(ptr) : v.big_containing(ptr);
+  if (!b) return false;
+  d->base = v.ptr(b);
+  d->size = b->bytes;
+  d->small = nullptr;
+  d->big = b;
+  return true;
 }
 
 int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
   if (!ptr) return LMS_OK;
   if (!c->vmm || !c->vmm->owns(ptr)) return fail(LMS_E_INVALID, "lms_dev_free: pointer not from the device pool");
-  Block* b = c->vmm->find_live(ptr);
-  if (!b) return fail(LMS_E_INVALID, "lms_dev_free: not a live allocation");
-  b->tag = stream;
+  DevBlk d;
+  if (!find_dev(c, ptr, true, &d)) return fail(LMS_E_INVALID, "lms_dev_free: not a live allocation");
+  d.stream = stream;
+  if (d.big) {
+    d.free_ev = c->events.get();
+    cudaEventRecord(d.free_ev, static_cast<cudaStream_t>(stream));
+  }
   c->st.n_free++;
-  if (!holds_clear(c, b)) {
-    c->deferred.push_back(b);
-    c->deferred_bytes += b->size;
+  if (!holds_clear(c, d.base)) {
+    c->deferred.push_back(d);
+    c->deferred_bytes += d.size;
     c->st.n_deferred_frees++;
     return LMS_OK;
   }
-  release_block(c, b);
+  release_block(c, d);
   return LMS_OK;
 }
 
@@ -721,7 +784,7 @@ int lms_set_limit(lms_ctx* c, size_t limit) {
 int lms_reset_peaks(lms_ctx* c) {
   std::lock_guard<std::mutex> g(c->mu);
   c->alloc_peak = c->alloc_bytes;
-  if (c->vmm) c->vmm->reset_mapped_peak();
+  c->mapped_peak = c->vmm ? c->vmm->mapped_bytes() : 0;
   c->host_peak = c->host_used;
   return LMS_OK;
 }
@@ -749,13 +812,13 @@ int lms_dev_hold_until(lms_ctx* c, const void* ptr, void* stream) {
   if (!c || !ptr) return fail(LMS_E_INVALID, "null argument");
   std::lock_guard<std::mutex> g(c->mu);
   if (!c->vmm || !c->vmm->owns(ptr)) return LMS_OK;  // not ours: nothing to hold
-  Block* b = c->vmm->containing(ptr);
-  if (!b) return fail(LMS_E_INVALID, "lms_dev_hold_until: pointer not in a live block");
+  DevBlk d;
+  if (!find_dev(c, ptr, false, &d)) return fail(LMS_E_INVALID, "lms_dev_hold_until: pointer not in a live block");
   auto* ev = new SharedEv();
   ev->e = c->events.get();
   ev->refs = 1;
   CK(cudaEventRecord(ev->e, static_cast<cudaStream_t>(stream)));
-  c->holds[b].push_back(ev);
+  c->holds[d.base].push_back(ev);
   return LMS_OK;
 }
 
@@ -841,10 +904,10 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
   }
   // hold the source block until the copy is done
   if (stored && c->vmm && c->vmm->owns(src)) {
-    Block* b = c->vmm->containing(src);
-    if (b) {
+    DevBlk d;
+    if (find_dev(c, src, false, &d)) {
       h->out_done->refs++;
-      c->holds[b].push_back(h->out_done);
+      c->holds[d.base].push_back(h->out_done);
     }
   }
   c->st.n_swap_out++;
@@ -1046,9 +1109,9 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   s.device_peak = c->alloc_peak;
   s.device_reserved = c->vmm ? c->vmm->va_bytes() : 0;
   s.device_limit = c->limit;
-  s.device_largest_free = c->vmm ? c->vmm->large_.largest_free() : 0;
+  s.device_cached = c->vmm ? c->vmm->cached_bytes() : 0;
   s.device_mapped = c->vmm ? c->vmm->mapped_bytes() : 0;
-  s.device_mapped_peak = c->vmm ? c->vmm->mapped_peak_bytes() : 0;
+  s.device_mapped_peak = c->mapped_peak;
   s.n_map = c->vmm ? c->vmm->n_map() : 0;
   s.n_unmap = c->vmm ? c->vmm->n_unmap() : 0;
   s.n_reclaims = c->n_reclaims;
@@ -1085,8 +1148,7 @@ int lms_live_blocks(lms_ctx* c, uint64_t* sizes, size_t cap, size_t* n) {
   std::lock_guard<std::mutex> g(c->mu);
   std::vector<uint64_t> v;
   if (c->vmm) {
-    c->vmm->small_.for_each_live([&](Block* b) { v.push_back(b->size); });
-    c->vmm->large_.for_each_live([&](Block* b) { v.push_back(b->size); });
+    c->vmm->for_each_live([&](uint64_t s) { v.push_back(s); });
   }
   std::sort(v.begin(), v.end(), std::greater<uint64_t>());
   size_t k = std::min(cap, v.size());

@@ -39,7 +39,7 @@ class _Config(ctypes.Structure):
 
 
 _STAT_FIELDS = [
-    "device_in_use", "device_peak", "device_reserved", "device_limit", "device_largest_free",
+    "device_in_use", "device_peak", "device_reserved", "device_limit", "device_cached",
     "device_deferred_bytes", "device_mapped", "device_mapped_peak", "n_map", "n_unmap", "n_reclaims", "n_device_syncs",
     "host_in_use", "host_peak", "host_reserved", "n_alloc", "n_free",
     "n_oom", "n_deferred_frees", "n_cross_stream_waits", "n_swap_out", "n_swap_in",

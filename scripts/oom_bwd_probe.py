@@ -19,8 +19,15 @@ for B in [int(a) for a in sys.argv[1:]]:
     x = torch.randn(B, 3, 224, 224, device="cuda"); y = torch.randint(0, 1000, (B,), device="cuda")
     t0 = time.time()
     try:
-        for _ in range(2):
-            lms.step(x, y)
+        for i in range(int(__import__("os").environ.get("STEPS", "2"))):
+            s0 = ctx.stats(); t1 = time.time()
+            lms.step(x, y); torch.cuda.synchronize()
+            s1 = ctx.stats()
+            d = {k: round(s1[k] - s0[k], 1) for k in ("n_map", "n_unmap", "n_reclaims", "n_device_syncs",
+                 "pool_driver_ms", "d2h_busy_ms", "h2d_busy_ms", "swap_wait_ms", "n_deferred_frees")}
+            d["GB_d2h"] = round((s1["d2h_wire_bytes"] - s0["d2h_wire_bytes"]) / 1e9, 2)
+            d["GB_h2d"] = round((s1["h2d_wire_bytes"] - s0["h2d_wire_bytes"]) / 1e9, 2)
+            print(B, "step", i, round(time.time() - t1, 3), "s", d, flush=True)
         print(B, "ok", round(time.time() - t0, 2), "s; peak", round(ctx.stats()["device_peak"] / 2**30, 2), flush=True)
     except RuntimeError as e:
         print(B, "OOM", "".join(traceback.format_exception_only(e))[:150].strip(), flush=True)
