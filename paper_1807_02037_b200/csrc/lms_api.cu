@@ -311,6 +311,9 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
   std::string err;
   const size_t rsize = Arena::round(size);
   if (size <= VmmPool::kSmallMax) {
+    if ((v.live_bytes() + rsize + v.page() - 1) / v.page() > c->limit / v.page()) reap_deferred(c, true);
+    if ((v.live_bytes() + rsize + v.page() - 1) / v.page() > c->limit / v.page())
+      return oom(c, size, "live set plus request exceeds the budget");
     for (int attempt = 0; attempt < 3; ++attempt) {
       if (attempt == 1) reap_deferred(c, true);
       if (attempt > 0) {
@@ -332,6 +335,19 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
     return oom(c, size, err);
   }
   const size_t pages = (rsize + v.page() - 1) / v.page();
+  const size_t limit_pages = c->limit / v.page();
+  // budget on live pages: the non-deferred live set can only shrink by frees
+  // the caller has not made yet, so if it plus this request is over the
+  // budget, fail now (cuDNN's plan loop probes oversized workspaces and
+  // expects a quick OOM); if only the deferred frees are in the way, wait
+  // for their swap-out copies
+  const size_t deferred_pages = (c->deferred_bytes + v.page() - 1) / v.page();
+  if (v.live_pages() - std::min(v.live_pages(), deferred_pages) + pages > limit_pages) {
+    drain_pool_events(c);
+    return oom(c, size, "live set plus request exceeds the budget");
+  }
+  if (v.live_pages() + pages > limit_pages) reap_deferred(c, true);
+  if (v.live_pages() + pages > limit_pages) return oom(c, size, "live set plus request exceeds the budget");
   bool needs_wait = false;
   Big* b = v.big_from_cache(pages, stream, &needs_wait);
   if (b) {
@@ -342,14 +358,6 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
     if (b->ev) c->events.put(b->ev);
     b->ev = nullptr;
   } else {
-    // the non-deferred live set can only shrink by frees the caller has not
-    // made yet: if it plus this request exceeds the budget, fail now (cuDNN's
-    // plan loop probes oversized workspaces and expects a quick OOM)
-    const size_t live_pages = (c->alloc_bytes - c->deferred_bytes + v.page() - 1) / v.page();
-    if (live_pages + pages > c->limit / v.page()) {
-      drain_pool_events(c);
-      return oom(c, size, "live set plus request exceeds the budget");
-    }
     b = v.big_fresh(rsize, pages, false, &err);
     if (!b && !c->deferred.empty()) {
       reap_deferred(c, true);
@@ -775,6 +783,13 @@ int lms_set_limit(lms_ctx* c, size_t limit) {
   if (c->vmm) {
     c->vmm->set_limit(limit);
     c->limit = c->vmm->limit_bytes();
+    if (c->vmm->mapped_bytes() > c->limit) {
+      // shrinking below what is mapped: drop the cache once nothing uses it
+      cudaDeviceSynchronize();
+      reap_deferred(c, true);
+      c->vmm->flush_cache();
+      drain_pool_events(c);
+    }
   } else {
     c->limit = limit;
   }

@@ -1,5 +1,6 @@
 """OOM inside a swapped backward: memory must come back."""
-import sys, gc, time, traceback
+import sys, gc, time, traceback, faulthandler
+faulthandler.dump_traceback_later(50, repeat=True)
 sys.path.insert(0, '.')
 import torch, torchvision
 from paper_1807_02037_b200 import runtime as rt, RewriteConfig
