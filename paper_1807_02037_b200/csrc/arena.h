@@ -8,10 +8,12 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <algorithm>
 #include <iterator>
 #include <map>
 #include <set>
 #include <utility>
+#include <vector>
 
 namespace lms {
 
@@ -23,6 +25,7 @@ struct Block {
   Block* next = nullptr;
   void* tag = nullptr;  // owner-defined (last-use stream for device blocks)
   class Arena* owner = nullptr;
+  uint64_t seq = 0;     // owner-defined: stream clock value when the block was freed
 };
 
 class Arena {
@@ -84,6 +87,7 @@ class Arena {
       rest->off = pick->off + size;
       rest->size = pick->size - size;
       rest->tag = pick->tag;
+      rest->seq = pick->seq;
       rest->prev = pick;
       rest->next = pick->next;
       if (pick->next) pick->next->prev = rest;
@@ -113,6 +117,8 @@ class Arena {
       Block* p = b->prev;
       free_.erase({p->size, p});
       if (p->tag == fresh_) p->tag = b->tag;
+      // same stream (or fresh): the later free stamp covers both
+      p->seq = std::max(p->seq, b->seq);
       p->size += b->size;
       p->next = b->next;
       if (b->next) b->next->prev = p;
@@ -123,6 +129,7 @@ class Arena {
       Block* n = b->next;
       free_.erase({n->size, n});
       if (b->tag == fresh_) b->tag = n->tag;
+      b->seq = std::max(b->seq, n->seq);
       b->size += n->size;
       b->next = n->next;
       if (n->next) n->next->prev = b;
@@ -230,6 +237,7 @@ class Arena {
 
   char* base_ = nullptr;
   size_t align_ = kAlign;
+
   void* fresh_ = nullptr;
   size_t cap_ = 0;
   Block* head_ = nullptr;

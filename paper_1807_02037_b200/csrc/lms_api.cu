@@ -97,14 +97,13 @@ struct XferRec {
   cudaEvent_t start, end;
 };
 
-// a live device allocation: small (arena block) or large (mapped VA range)
+// a device allocation on its way back to the pool
 struct DevBlk {
   char* base = nullptr;
   size_t size = 0;
-  Block* small = nullptr;
-  Big* big = nullptr;
-  void* stream = nullptr;          // freeing stream (deferred blocks)
-  cudaEvent_t free_ev = nullptr;   // recorded at free on that stream (large blocks)
+  Block* blk = nullptr;
+  void* stream = nullptr;   // freeing stream
+  uint64_t seq = 0;         // that stream's clock at the free
 };
 
 }  // namespace lms
@@ -208,20 +207,10 @@ bool holds_clear(lms_ctx* c, char* base) {
   return false;
 }
 
-void drain_pool_events(lms_ctx* c) {
-  for (auto e : c->vmm->events_done_) c->events.put(e);
-  c->vmm->events_done_.clear();
-}
-
-// give a freed block back to the pool (large blocks go to the mapped cache)
+// give a freed block back to the pool
 void release_block(lms_ctx* c, const DevBlk& d) {
   c->alloc_bytes -= d.size;
-  if (d.small) {
-    d.small->tag = d.stream;
-    c->vmm->small_free(d.small);
-  } else {
-    c->vmm->big_free(d.big, d.stream, d.free_ev);
-  }
+  c->vmm->free(d.blk, d.stream, d.seq);
 }
 
 void reap_deferred(lms_ctx* c, bool block) {
@@ -253,7 +242,7 @@ void stream_wait_on(lms_ctx* c, void* waiter, void* owner) {
 
 int ensure_pool(lms_ctx* c) {
   if (c->vmm) return LMS_OK;
-  size_t limit = c->cfg.device_limit ? c->cfg.device_limit : c->cfg.device_reserve;
+  size_t limit = c->cfg.device_reserve ? c->cfg.device_reserve : c->cfg.device_limit;
   if (limit == 0) {
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
@@ -261,24 +250,14 @@ int ensure_pool(lms_ctx* c) {
   }
   auto* v = new VmmPool();
   std::string err;
-  if (!v->init(c->device, limit, 4 * limit, kFresh, &err)) {
-    delete v;
-    return fail(LMS_E_CUDA, "device pool: " + err);
-  }
-  if (c->cfg.device_reserve && !v->precreate(c->cfg.device_reserve / v->page(), &err)) {
+  if (!v->init(c->device, limit, kFresh, &err)) {
     delete v;
     return fail(LMS_E_CUDA, "device pool: " + err);
   }
   c->vmm = v;
-  c->limit = v->limit_bytes();
+  c->limit = c->cfg.device_limit && c->cfg.device_limit < v->limit_bytes() ? c->cfg.device_limit
+                                                                            : v->limit_bytes();
   return LMS_OK;
-}
-
-void note_alloc(lms_ctx* c, size_t bytes) {
-  c->st.n_alloc++;
-  c->alloc_bytes += bytes;
-  c->alloc_peak = std::max(c->alloc_peak, c->alloc_bytes);
-  c->mapped_peak = std::max(c->mapped_peak, c->vmm->mapped_bytes());
 }
 
 int oom(lms_ctx* c, size_t size, const std::string& why) {
@@ -288,8 +267,8 @@ int oom(lms_ctx* c, size_t size, const std::string& why) {
     std::vector<uint64_t> sz;
     v.for_each_live([&](uint64_t s) { sz.push_back(s); });
     std::sort(sz.begin(), sz.end(), std::greater<uint64_t>());
-    fprintf(stderr, "[lms] OOM wanting %zu B: %zu live blocks, deferred %zu B, cached %zu B, largest:", size,
-            sz.size(), c->deferred_bytes, v.cached_bytes());
+    fprintf(stderr, "[lms] OOM wanting %zu B: %zu live blocks, deferred %zu B, largest:", size, sz.size(),
+            c->deferred_bytes);
     for (size_t i = 0; i < sz.size() && i < 16; ++i) fprintf(stderr, " %.0fM", sz[i] / 1048576.0);
     fprintf(stderr, "\n");
   }
@@ -300,96 +279,58 @@ int oom(lms_ctx* c, size_t size, const std::string& why) {
   return fail(LMS_E_OOM, buf);
 }
 
-// returns LMS_OK and *out, or LMS_E_OOM.  Escalation when pages are short:
-// evict finished cached blocks, then wait for deferred frees (pending
-// swap-out copies), then wait for unfinished cached blocks.
+// returns LMS_OK and *out, or LMS_E_OOM.  The budget is on live pages; when
+// it is short only because freed blocks still wait for their swap-out copies
+// the call blocks until those copies land (this is what throttles a forward
+// pass that outruns the D2H channel).
 int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
   int rc = ensure_pool(c);
   if (rc) return rc;
   VmmPool& v = *c->vmm;
   reap_deferred(c, false);
-  std::string err;
-  const size_t rsize = Arena::round(size);
-  if (size <= VmmPool::kSmallMax) {
-    if ((v.live_bytes() + rsize + v.page() - 1) / v.page() > c->limit / v.page()) reap_deferred(c, true);
-    if ((v.live_bytes() + rsize + v.page() - 1) / v.page() > c->limit / v.page())
-      return oom(c, size, "live set plus request exceeds the budget");
-    for (int attempt = 0; attempt < 3; ++attempt) {
-      if (attempt == 1) reap_deferred(c, true);
-      if (attempt > 0) {
-        // a small block spans at most two pages: evict cache for them
-        v.make_room(2, attempt == 2);
-        drain_pool_events(c);
-      }
-      Block* b = v.small_alloc(size, stream, &err);
-      if (b) {
-        void* prev = b->tag;
-        if (prev != kFresh && prev != stream) stream_wait_on(c, stream, prev);
-        b->tag = stream;
-        note_alloc(c, b->size);
-        *out = v.small_ptr(b);
-        return LMS_OK;
-      }
-    }
-    drain_pool_events(c);
-    return oom(c, size, err);
-  }
-  const size_t pages = (rsize + v.page() - 1) / v.page();
-  const size_t limit_pages = c->limit / v.page();
-  // budget on live pages: the non-deferred live set can only shrink by frees
-  // the caller has not made yet, so if it plus this request is over the
-  // budget, fail now (cuDNN's plan loop probes oversized workspaces and
-  // expects a quick OOM); if only the deferred frees are in the way, wait
-  // for their swap-out copies
-  const size_t deferred_pages = (c->deferred_bytes + v.page() - 1) / v.page();
-  if (v.live_pages() - std::min(v.live_pages(), deferred_pages) + pages > limit_pages) {
-    drain_pool_events(c);
+  const size_t page = v.page();
+  const size_t want = (Arena::round(size) + page - 1) / page;
+  const size_t limit_pages = c->limit / page;
+  const size_t deferred_pages = (c->deferred_bytes + page - 1) / page;
+  const size_t live = v.live_pages();
+  // the non-deferred live set only shrinks by frees the caller has not made
+  // yet: fail at once (cuDNN's plan loop probes oversized workspaces)
+  if (live - std::min(live, deferred_pages) + want > limit_pages)
     return oom(c, size, "live set plus request exceeds the budget");
+  if (live + want > limit_pages) reap_deferred(c, true);
+  if (v.live_pages() + want > limit_pages) return oom(c, size, "live set plus request exceeds the budget");
+  std::string err;
+  Block* b = v.alloc(size, stream, false, &err);
+  if (!b && !c->deferred.empty()) {
+    reap_deferred(c, true);
+    err.clear();
+    b = v.alloc(size, stream, false, &err);
   }
-  if (v.live_pages() + pages > limit_pages) reap_deferred(c, true);
-  if (v.live_pages() + pages > limit_pages) return oom(c, size, "live set plus request exceeds the budget");
-  bool needs_wait = false;
-  Big* b = v.big_from_cache(pages, stream, &needs_wait);
-  if (b) {
-    if (needs_wait) {
-      CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), b->ev, 0));
-      c->st.n_cross_stream_waits++;
-    }
-    if (b->ev) c->events.put(b->ev);
-    b->ev = nullptr;
-  } else {
-    b = v.big_fresh(rsize, pages, false, &err);
-    if (!b && !c->deferred.empty()) {
-      reap_deferred(c, true);
-      b = v.big_fresh(rsize, pages, false, &err);
-    }
-    if (!b) b = v.big_fresh(rsize, pages, true, &err);
-    drain_pool_events(c);
-    if (!b) return oom(c, size, err);
+  if (!b) {
+    err.clear();
+    b = v.alloc(size, stream, true, &err);
   }
-  v.big_live(b, rsize);
-  note_alloc(c, rsize);
+  if (!b) return oom(c, size, err);
+  // a range last used by another stream: wait for that use on the device
+  if (b->tag != kFresh && b->tag != stream && !v.idle(b)) {
+    v.clocks_.device_wait(stream, b->tag, b->seq);
+    c->st.n_cross_stream_waits++;
+  }
+  b->tag = stream;
+  c->st.n_alloc++;
+  c->alloc_bytes += b->size;
+  c->alloc_peak = std::max(c->alloc_peak, c->alloc_bytes);
+  c->mapped_peak = std::max(c->mapped_peak, v.mapped_bytes());
   *out = v.ptr(b);
   return LMS_OK;
 }
 
 bool find_dev(lms_ctx* c, const void* ptr, bool exact, DevBlk* d) {
-  VmmPool& v = *c->vmm;
-  if (v.is_small(ptr)) {
-    Block* b = exact ? v.small_find(ptr) : v.small_containing(ptr);
-    if (!b) return false;
-    d->base = v.small_ptr(b);
-    d->size = b->size;
-    d->small = b;
-    d->big = nullptr;
-    return true;
-  }
-  Big* b = exact ? v.big_find(ptr) : v.big_containing(ptr);
+  Block* b = exact ? c->vmm->find(ptr) : c->vmm->containing(ptr);
   if (!b) return false;
-  d->base = v.ptr(b);
-  d->size = b->bytes;
-  d->small = nullptr;
-  d->big = b;
+  d->base = c->vmm->ptr(b);
+  d->size = b->size;
+  d->blk = b;
   return true;
 }
 
@@ -399,10 +340,7 @@ int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
   DevBlk d;
   if (!find_dev(c, ptr, true, &d)) return fail(LMS_E_INVALID, "lms_dev_free: not a live allocation");
   d.stream = stream;
-  if (d.big) {
-    d.free_ev = c->events.get();
-    cudaEventRecord(d.free_ev, static_cast<cudaStream_t>(stream));
-  }
+  d.seq = c->vmm->clocks_.stamp(stream);
   c->st.n_free++;
   if (!holds_clear(c, d.base)) {
     c->deferred.push_back(d);
@@ -781,15 +719,8 @@ int lms_set_limit(lms_ctx* c, size_t limit) {
   if (limit == 0) limit = c->cfg.device_reserve ? c->cfg.device_reserve : c->limit;
   c->cfg.device_limit = limit;
   if (c->vmm) {
-    c->vmm->set_limit(limit);
-    c->limit = c->vmm->limit_bytes();
-    if (c->vmm->mapped_bytes() > c->limit) {
-      // shrinking below what is mapped: drop the cache once nothing uses it
-      cudaDeviceSynchronize();
-      reap_deferred(c, true);
-      c->vmm->flush_cache();
-      drain_pool_events(c);
-    }
+    // physical pages are fixed at creation; the budget on live pages moves
+    c->limit = std::min(limit, c->vmm->limit_bytes());
   } else {
     c->limit = limit;
   }
@@ -1124,12 +1055,12 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   s.device_peak = c->alloc_peak;
   s.device_reserved = c->vmm ? c->vmm->va_bytes() : 0;
   s.device_limit = c->limit;
-  s.device_cached = c->vmm ? c->vmm->cached_bytes() : 0;
+  s.device_cached = c->vmm ? c->vmm->mapped_bytes() - std::min(c->vmm->mapped_bytes(), c->alloc_bytes) : 0;
   s.device_mapped = c->vmm ? c->vmm->mapped_bytes() : 0;
   s.device_mapped_peak = c->mapped_peak;
   s.n_map = c->vmm ? c->vmm->n_map() : 0;
   s.n_unmap = c->vmm ? c->vmm->n_unmap() : 0;
-  s.n_reclaims = c->n_reclaims;
+  s.n_reclaims = c->vmm ? c->vmm->n_moves() : 0;
   s.n_device_syncs = c->n_device_syncs;
   s.pool_driver_ms = c->vmm ? c->vmm->driver_ms() : 0;
   s.device_deferred_bytes = c->deferred_bytes;

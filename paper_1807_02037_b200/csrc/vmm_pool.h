@@ -1,23 +1,19 @@
 // Device pool over CUDA virtual memory: the budget caps PHYSICAL pages.
 //
-// Physical memory is a fixed set of pages (the driver's allocation
-// granularity, 2 MiB on B200) created once, up front, up to the budget.
-// Virtual address space is reserved generously and never limits anything.
+// The budget's worth of physical pages (the driver's allocation granularity,
+// 2 MiB on B200) is created and mapped once, contiguously, at the start of a
+// much larger reserved VA range.  Two best-fit arenas carve the VA: small
+// blocks (<= 1 MiB, 512 B granules, several per page) and large blocks
+// (page-aligned).  While the mapped region has a free range that fits, this
+// is an ordinary caching allocator: split and merge in place, no driver call.
+// Only when fragmentation leaves no mapped range large enough does the pool
+// move pages: it unmaps idle pages of free ranges and maps them under a free
+// VA range that fits (usually the unmapped tail), so a request that fits the
+// budget never fails for lack of contiguity.
 //
-// * Large blocks (> 1 MiB) get their own page-aligned VA range with pages
-//   mapped in.  A freed large block stays mapped in an exact-size cache with
-//   the event recorded at free: a training step allocates the same multiset
-//   of sizes every iteration, so steady-state allocation is a cache hit with
-//   no driver call.  When an allocation needs pages and none are free, the
-//   least recently freed cached block whose event has completed is unmapped
-//   (its VA range goes back to the VA arena, its pages to the free list); no
-//   device-wide synchronisation is needed because each cached block knows
-//   when its last user finished.
-// * Small blocks (<= 1 MiB) are sub-allocated from a dedicated VA region
-//   whose pages are mapped on first use and stay mapped.
-//
-// A hole in VA therefore never wastes HBM, and a step fits the budget iff its
-// live bytes (rounded to pages) do: fragmentation cannot cause an OOM.
+// "Idle" is decided without device-wide synchronisation: every free records
+// an event on the freeing stream and stamps the block with that stream's
+// clock value; a block is idle once its stream's clock has passed the stamp.
 //
 // Driver entry points come from cudaGetDriverEntryPoint (no link-time libcuda).
 #pragma once
@@ -28,9 +24,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
-#include <list>
-#include <map>
+#include <deque>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "arena.h"
@@ -65,15 +61,74 @@ struct Drv {
   }
 };
 
-// one large block: a VA range (owned by the VA arena) with `pages` mapped
-struct Big {
-  Block* va = nullptr;      // range in the VA arena
-  size_t pages = 0;
-  size_t bytes = 0;         // requested size rounded to 512 B
-  void* stream = nullptr;   // last user
-  cudaEvent_t ev = nullptr; // recorded when freed; completes when the last user is done
-  std::list<Big*>::iterator lru;
-  std::vector<int> handles; // physical page per VA page
+// Per-stream logical clock: stamp() records an event and returns a number;
+// passed(s) says whether all work enqueued before stamp s has finished.
+class StreamClocks {
+ public:
+  ~StreamClocks() {
+    for (auto& kv : clocks_)
+      for (auto& p : kv.second.pending) cudaEventDestroy(p.second);
+    for (auto e : spare_) cudaEventDestroy(e);
+  }
+  uint64_t stamp(void* stream) {
+    Clock& c = clocks_[stream];
+    cudaEvent_t e;
+    if (!spare_.empty()) {
+      e = spare_.back();
+      spare_.pop_back();
+    } else {
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    cudaEventRecord(e, static_cast<cudaStream_t>(stream));
+    uint64_t s = ++c.next;
+    c.pending.emplace_back(s, e);
+    if (c.pending.size() > 64) poll(c);
+    return s;
+  }
+  bool passed(void* stream, uint64_t s) {
+    if (s == 0) return true;
+    auto it = clocks_.find(stream);
+    if (it == clocks_.end()) return true;
+    Clock& c = it->second;
+    if (c.done >= s) return true;
+    poll(c);
+    return c.done >= s;
+  }
+  // block the host until stamp s on `stream` has passed
+  void wait(void* stream, uint64_t s) {
+    auto it = clocks_.find(stream);
+    if (it == clocks_.end()) return;
+    Clock& c = it->second;
+    while (c.done < s && !c.pending.empty()) {
+      cudaEventSynchronize(c.pending.front().second);
+      poll(c);
+    }
+  }
+  // make `waiter` wait (on the device) for stamp s of `stream`
+  void device_wait(void* waiter, void* stream, uint64_t s) {
+    auto it = clocks_.find(stream);
+    if (it == clocks_.end()) return;
+    for (auto& p : it->second.pending)
+      if (p.first >= s) {
+        cudaStreamWaitEvent(static_cast<cudaStream_t>(waiter), p.second, 0);
+        return;
+      }
+  }
+
+ private:
+  struct Clock {
+    std::deque<std::pair<uint64_t, cudaEvent_t>> pending;
+    uint64_t next = 0, done = 0;
+  };
+  void poll(Clock& c) {
+    while (!c.pending.empty() && cudaEventQuery(c.pending.front().second) == cudaSuccess) {
+      c.done = c.pending.front().first;
+      spare_.push_back(c.pending.front().second);
+      c.pending.pop_front();
+    }
+  }
+  std::unordered_map<void*, Clock> clocks_;
+  std::vector<cudaEvent_t> spare_;
 };
 
 class VmmPool {
@@ -82,8 +137,11 @@ class VmmPool {
 
   ~VmmPool() { teardown(); }
 
-  bool init(int device, size_t limit_bytes, size_t va_bytes, void* fresh, std::string* err) {
+  // reserve VA, create `limit_bytes` of pages and map them at the start of
+  // the large region
+  bool init(int device, size_t limit_bytes, void* fresh, std::string* err) {
     if (!drv_.load(err)) return false;
+    fresh_ = fresh;
     prop_ = CUmemAllocationProp{};
     prop_.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop_.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -94,9 +152,9 @@ class VmmPool {
       return false;
     }
     page_ = g;
+    limit_pages_ = limit_bytes / page_;
     small_va_ = size_t(8) << 30;
-    large_va_ = std::max(va_bytes, size_t(64) << 30);
-    large_va_ = (large_va_ + page_ - 1) / page_ * page_;
+    large_va_ = std::max(4 * limit_pages_ * page_, size_t(64) << 30);
     CUdeviceptr base = 0;
     if (drv_.reserve(&base, small_va_ + large_va_, page_, 0, 0) != CUDA_SUCCESS) {
       *err = "cuMemAddressReserve failed";
@@ -104,208 +162,106 @@ class VmmPool {
     }
     base_ = reinterpret_cast<char*>(base);
     small_.init(base_, small_va_, fresh, Arena::kAlign);
-    va_.init(base_ + small_va_, large_va_, nullptr, page_);
-    small_pages_.assign(small_va_ / page_, -1);
-    small_live_.assign(small_va_ / page_, 0);
+    large_.init(base_ + small_va_, large_va_, fresh, page_);
+    handle_of_.assign((small_va_ + large_va_) / page_, -1);
+    live_.assign(handle_of_.size(), 0);
     access_.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     access_.location.id = device;
     access_.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    set_limit(limit_bytes);
-    return true;
-  }
-
-  // create physical pages up front (cuMemCreate is the slow driver call)
-  bool precreate(size_t pages, std::string* err) {
     auto t0 = now();
-    while (created_ < std::min(pages, limit_pages_)) {
+    for (size_t i = 0; i < limit_pages_; ++i) {
       CUmemGenericAllocationHandle hd = 0;
       if (drv_.create(&hd, page_, &prop_, 0) != CUDA_SUCCESS) {
-        *err = "cuMemCreate failed while pre-creating pages";
-        driver_s_ += secs(t0);
+        *err = "cuMemCreate failed (not enough device memory for the budget?)";
         return false;
       }
       handles_.push_back(hd);
-      free_.push_back(int(handles_.size()) - 1);
-      ++created_;
+      free_.push_back(int(i));
     }
+    created_ = limit_pages_;
     driver_s_ += secs(t0);
-    return true;
+    // map the whole budget contiguously at the start of the large region
+    size_t first = small_va_ / page_;
+    std::vector<size_t> pages(limit_pages_);
+    for (size_t i = 0; i < limit_pages_; ++i) pages[i] = first + i;
+    return map_pages(pages, err);
   }
 
-  void set_limit(size_t bytes) { limit_pages_ = bytes / page_; }
-  size_t limit_bytes() const { return limit_pages_ * page_; }
   size_t page() const { return page_; }
+  size_t limit_bytes() const { return limit_pages_ * page_; }
   char* base() const { return base_; }
   bool owns(const void* p) const {
     const char* c = static_cast<const char*>(p);
     return base_ && c >= base_ && c < base_ + small_va_ + large_va_;
   }
-  bool is_small(const void* p) const { return static_cast<const char*>(p) < base_ + small_va_; }
+  Arena& arena_for(size_t size) { return size <= kSmallMax ? small_ : large_; }
+  Arena& arena_of(const void* p) { return static_cast<const char*>(p) < base_ + small_va_ ? small_ : large_; }
+  char* ptr(const Block* b) const { return b->owner->base() + b->off; }
+  Block* find(const void* p) {
+    Arena& a = arena_of(p);
+    return a.find_live(static_cast<const char*>(p) - a.base());
+  }
+  Block* containing(const void* p) {
+    Arena& a = arena_of(p);
+    return a.containing(static_cast<const char*>(p) - a.base());
+  }
 
-  // ---- small blocks -------------------------------------------------------
-  // nullptr when pages are short (the caller evicts or waits and retries)
-  Block* small_alloc(size_t size, void* stream, std::string* err) {
-    Block* b = small_.alloc(size, stream);
+  // Allocate `size` bytes for `stream`.  On success the block is live and
+  // backed; *wait_stream/*wait_seq name a stamp the caller's stream must
+  // device-wait on (cross-stream reuse of a range not yet idle), or null.
+  Block* alloc(size_t size, void* stream, bool may_block, std::string* err) {
+    Arena& ar = arena_for(size);
+    Block* b = ar.alloc_scored(size, [&](const Block* fb, size_t sz) -> long {
+      long unmapped = long(unmapped_in(ar, fb->off, sz));
+      long foreign = (fb->tag != stream && fb->tag != fresh_) ? 1 : 0;
+      return 4 * unmapped + foreign;
+    });
     if (!b) {
-      *err = "small-block VA exhausted";
+      *err = "VA exhausted";
       return nullptr;
     }
-    size_t f = b->off / page_, l = (b->off + b->size - 1) / page_;
-    size_t need = 0;
-    for (size_t p = f; p <= l; ++p) need += small_pages_[p] < 0;
-    if (need > spare_pages()) {
-      small_.release(b);
-      *err = "physical page budget exhausted";
+    pin(b, +1);
+    size_t f, l;
+    span(b, &f, &l);
+    std::vector<size_t> need;
+    for (size_t p = f; p <= l; ++p)
+      if (handle_of_[p] < 0) need.push_back(p);
+    if (!need.empty() && !(steal(need.size(), may_block) && map_pages(need, err))) {
+      pin(b, -1);
+      ar.release(b);
+      if (err->empty()) *err = "physical page budget exhausted (no idle pages to move)";
       return nullptr;
     }
-    for (size_t p = f; p <= l; ++p) {
-      if (small_pages_[p] < 0) {
-        int h = take_page();
-        if (!map_pages(base_ + p * page_, &h, 1, err)) {
-          give_page(h);
-          for (size_t q = f; q < p; ++q) --small_live_[q];
-          small_.release(b);
-          return nullptr;
-        }
-        small_pages_[p] = h;
-        ++small_mapped_;
-      }
-      ++small_live_[p];
-    }
-    small_bytes_ += b->size;
-    return b;
-  }
-  void small_free(Block* b) {
-    size_t f = b->off / page_, l = (b->off + b->size - 1) / page_;
-    for (size_t p = f; p <= l; ++p) --small_live_[p];
-    small_bytes_ -= b->size;
-    small_.release(b);
-  }
-  Block* small_find(const void* p) { return small_.find_live(static_cast<const char*>(p) - base_); }
-  Block* small_containing(const void* p) { return small_.containing(static_cast<const char*>(p) - base_); }
-  char* small_ptr(const Block* b) const { return base_ + b->off; }
-  Arena& small_arena() { return small_; }
-
-  // ---- large blocks --------------------------------------------------------
-  // exact-size cache hit: the caller's stream first (stream order makes the
-  // reuse safe), then a block whose last user finished, then any (the caller
-  // must make its stream wait on the returned block's event)
-  Big* big_from_cache(size_t pages, void* stream, bool* needs_wait) {
-    auto range = cache_.equal_range(pages);
-    auto done = cache_.end(), any = cache_.end();
-    for (auto it = range.first; it != range.second; ++it) {
-      Big* b = it->second;
-      if (b->stream == stream) return take_cached(it, needs_wait, false);
-      if (done == cache_.end() && (b->ev == nullptr || cudaEventQuery(b->ev) == cudaSuccess)) done = it;
-      if (any == cache_.end()) any = it;
-    }
-    if (done != cache_.end()) return take_cached(done, needs_wait, false);
-    if (any != cache_.end()) return take_cached(any, needs_wait, true);
-    return nullptr;
-  }
-
-  // fresh VA + pages, evicting finished cached blocks for pages (waiting for
-  // unfinished ones only if `wait_for_cache`).  nullptr if the budget cannot
-  // supply `pages`.
-  Big* big_fresh(size_t bytes, size_t pages, bool wait_for_cache, std::string* err) {
-    while (spare_pages() < pages) {
-      if (!evict_one(wait_for_cache)) {
-        *err = "physical page budget exhausted";
-        return nullptr;
-      }
-    }
-    Block* va = va_.alloc(pages * page_);
-    if (!va) {
-      *err = "large-block VA exhausted";
-      return nullptr;
-    }
-    Big* b = new Big();
-    b->va = va;
-    b->pages = pages;
-    b->bytes = bytes;
-    b->handles.resize(pages);
-    for (size_t i = 0; i < pages; ++i) b->handles[i] = take_page();
-    if (!map_pages(va_.base() + va->off, b->handles.data(), pages, err)) {
-      for (int h : b->handles) give_page(h);
-      va_.release(va);
-      delete b;
-      return nullptr;
-    }
-    big_mapped_ += pages;
+    bytes_live_ += b->size;
     return b;
   }
 
-  void big_live(Big* b, size_t bytes) {
-    b->bytes = bytes;
-    live_[ptr(b)] = b;
-    big_live_pages_ += b->pages;
-    big_bytes_ += b->bytes;
+  void free(Block* b, void* stream, uint64_t seq) {
+    bytes_live_ -= b->size;
+    pin(b, -1);
+    b->tag = stream;
+    b->seq = seq;
+    b->owner->release(b);
   }
 
-  // freed by `stream`: cache it, with `ev` marking its last use
-  void big_free(Big* b, void* stream, cudaEvent_t ev) {
-    live_.erase(ptr(b));
-    big_live_pages_ -= b->pages;
-    big_bytes_ -= b->bytes;
-    b->stream = stream;
-    b->ev = ev;
-    lru_.push_back(b);
-    b->lru = std::prev(lru_.end());
-    cache_.emplace(b->pages, b);
-  }
+  // cross-stream reuse check for a freshly allocated block (before retagging)
+  bool idle(const Block* b) { return b->tag == fresh_ || clocks_.passed(b->tag, b->seq); }
 
-  Big* big_find(const void* p) {
-    auto it = live_.find(const_cast<char*>(static_cast<const char*>(p)));
-    return it == live_.end() ? nullptr : it->second;
-  }
-  Big* big_containing(const void* p) {
-    char* c = const_cast<char*>(static_cast<const char*>(p));
-    auto it = live_.upper_bound(c);
-    if (it == live_.begin()) return nullptr;
-    --it;
-    return c < it->first + it->second->pages * page_ ? it->second : nullptr;
-  }
-  char* ptr(const Big* b) const { return va_.base() + b->va->off; }
-
-  // evict cached blocks until `pages` pages are spare
-  bool make_room(size_t pages, bool wait) {
-    while (spare_pages() < pages)
-      if (!evict_one(wait)) return false;
-    return true;
-  }
-
-  // unmap every cached block (only when no cached block can be in use)
-  void flush_cache() {
-    while (!lru_.empty()) evict(lru_.front());
-  }
-  bool has_cache() const { return !lru_.empty(); }
-
-  // ---- accounting ------------------------------------------------------------
-  size_t mapped_pages() const { return small_mapped_ + big_mapped_; }
-  size_t spare_pages() const {
-    size_t m = mapped_pages();
-    if (m >= limit_pages_) return 0;
-    size_t creatable = created_ < limit_pages_ ? limit_pages_ - created_ : 0;
-    return std::min(limit_pages_ - m, free_.size() + creatable);
-  }
-  size_t live_pages() const { return big_live_pages_ + (small_bytes_ + page_ - 1) / page_; }
-  size_t live_bytes() const { return big_bytes_ + small_bytes_; }
-  size_t mapped_bytes() const { return mapped_pages() * page_; }
-  size_t cached_bytes() const { return (big_mapped_ - big_live_pages_) * page_; }
+  size_t live_bytes() const { return bytes_live_; }
+  size_t live_pages() const { return live_pages_; }
+  size_t mapped_bytes() const { return mapped_ * page_; }
   uint64_t n_map() const { return n_map_; }
   uint64_t n_unmap() const { return n_unmap_; }
-  uint64_t n_hits() const { return n_hits_; }
+  uint64_t n_moves() const { return n_moves_; }
   double driver_ms() const { return driver_s_ * 1e3; }
   size_t va_bytes() const { return small_va_ + large_va_; }
-  size_t largest_free_va() const { return va_.largest_free(); }
   template <class F>
   void for_each_live(F&& f) {
     small_.for_each_live([&](Block* b) { f(uint64_t(b->size)); });
-    for (auto& kv : live_) f(uint64_t(kv.second->bytes));
+    large_.for_each_live([&](Block* b) { f(uint64_t(b->size)); });
   }
 
-  // events of evicted blocks, handed back to the owner's event pool
-  std::vector<cudaEvent_t> events_done_;
+  StreamClocks clocks_;
 
  private:
   static std::chrono::steady_clock::time_point now() { return std::chrono::steady_clock::now(); }
@@ -313,99 +269,104 @@ class VmmPool {
     return std::chrono::duration<double>(now() - t0).count();
   }
 
-  Big* take_cached(std::multimap<size_t, Big*>::iterator it, bool* needs_wait, bool wait) {
-    Big* b = it->second;
-    cache_.erase(it);
-    lru_.erase(b->lru);
-    *needs_wait = wait;
-    ++n_hits_;
-    return b;
+  void span(const Block* b, size_t* f, size_t* l) const {
+    size_t lo = size_t(b->owner->base() - base_) + b->off;
+    *f = lo / page_;
+    *l = (lo + b->size - 1) / page_;
+  }
+  size_t unmapped_in(const Arena& a, size_t off, size_t size) const {
+    size_t lo = size_t(a.base() - base_) + off;
+    size_t f = lo / page_, l = (lo + a.round_up(size) - 1) / page_, n = 0;
+    for (size_t p = f; p <= l; ++p) n += handle_of_[p] < 0;
+    return n;
+  }
+  void pin(const Block* b, int d) {
+    size_t f, l;
+    span(b, &f, &l);
+    for (size_t p = f; p <= l; ++p) {
+      uint32_t before = live_[p];
+      live_[p] = uint32_t(int(before) + d);
+      live_pages_ += (before == 0 && live_[p] > 0) - (before > 0 && live_[p] == 0);
+    }
   }
 
-  int take_page() {
-    if (!free_.empty()) {
+  // make `n` pages free by unmapping idle pages of free ranges (no live
+  // block on them, last user finished); optionally wait for busy ones
+  bool steal(size_t n, bool may_block) {
+    if (free_.size() >= n) return true;
+    ++n_moves_;
+    for (int pass = 0; pass < 2 && free_.size() < n; ++pass) {
+      if (pass == 1 && !may_block) break;
+      std::vector<Block*> cands;
+      auto collect = [&](Block* fb) { cands.push_back(fb); };
+      large_.for_each_free(collect);
+      small_.for_each_free(collect);
+      // smallest ranges first: they are the fragments nobody can use
+      std::sort(cands.begin(), cands.end(), [](const Block* a, const Block* b) { return a->size < b->size; });
+      for (Block* fb : cands) {
+        if (free_.size() >= n) break;
+        if (fb->tag != fresh_ && !clocks_.passed(fb->tag, fb->seq)) {
+          if (pass == 0) continue;
+          clocks_.wait(fb->tag, fb->seq);
+        }
+        size_t f, l;
+        span(fb, &f, &l);
+        // only pages the free range owns entirely and no live block touches
+        for (size_t p = l + 1; p-- > f && free_.size() < n;) {
+          if (handle_of_[p] >= 0 && live_[p] == 0) unmap_page(p);
+        }
+      }
+    }
+    return free_.size() >= n;
+  }
+
+  void unmap_page(size_t p) {
+    auto t0 = now();
+    drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
+    driver_s_ += secs(t0);
+    free_.push_back(handle_of_[p]);
+    handle_of_[p] = -1;
+    --mapped_;
+    ++n_unmap_;
+  }
+
+  bool map_pages(const std::vector<size_t>& pages, std::string* err) {
+    auto t0 = now();
+    size_t run = 0;
+    for (size_t i = 0; i < pages.size(); ++i) {
       int h = free_.back();
       free_.pop_back();
-      return h;
-    }
-    CUmemGenericAllocationHandle hd = 0;
-    if (created_ >= limit_pages_ || drv_.create(&hd, page_, &prop_, 0) != CUDA_SUCCESS) return -1;
-    handles_.push_back(hd);
-    ++created_;
-    return int(handles_.size()) - 1;
-  }
-  void give_page(int h) {
-    if (h >= 0) free_.push_back(h);
-  }
-
-  bool map_pages(char* va, const int* hs, size_t n, std::string* err) {
-    auto t0 = now();
-    for (size_t i = 0; i < n; ++i) {
-      if (hs[i] < 0 || drv_.map(reinterpret_cast<CUdeviceptr>(va + i * page_), page_, 0, handles_[hs[i]], 0) !=
-                           CUDA_SUCCESS) {
-        for (size_t j = 0; j < i; ++j) drv_.unmap(reinterpret_cast<CUdeviceptr>(va + j * page_), page_);
+      size_t p = pages[i];
+      if (drv_.map(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_, 0, handles_[h], 0) != CUDA_SUCCESS) {
+        free_.push_back(h);
         *err = "cuMemMap failed";
         driver_s_ += secs(t0);
         return false;
       }
-    }
-    n_map_ += n;
-    bool ok = drv_.set_access(reinterpret_cast<CUdeviceptr>(va), n * page_, &access_, 1) == CUDA_SUCCESS;
-    if (!ok) *err = "cuMemSetAccess failed";
-    driver_s_ += secs(t0);
-    return ok;
-  }
-
-  void evict(Big* b) {
-    auto t0 = now();
-    char* va = ptr(b);
-    for (size_t i = 0; i < b->pages; ++i) drv_.unmap(reinterpret_cast<CUdeviceptr>(va + i * page_), page_);
-    driver_s_ += secs(t0);
-    n_unmap_ += b->pages;
-    for (int h : b->handles) give_page(h);
-    big_mapped_ -= b->pages;
-    auto range = cache_.equal_range(b->pages);
-    for (auto it = range.first; it != range.second; ++it)
-      if (it->second == b) {
-        cache_.erase(it);
-        break;
-      }
-    lru_.erase(b->lru);
-    va_.release(b->va);
-    if (b->ev) events_done_.push_back(b->ev);
-    delete b;
-  }
-
-  // evict the least recently freed cached block whose last user finished
-  // (or, if `wait`, the oldest one after waiting for it)
-  bool evict_one(bool wait) {
-    for (Big* b : lru_) {
-      if (b->ev == nullptr || cudaEventQuery(b->ev) == cudaSuccess) {
-        evict(b);
-        return true;
+      handle_of_[p] = h;
+      ++mapped_;
+      ++n_map_;
+      bool last = i + 1 == pages.size() || pages[i + 1] != p + 1;
+      if (last) {
+        size_t start = pages[run];
+        if (drv_.set_access(reinterpret_cast<CUdeviceptr>(base_ + start * page_), (p - start + 1) * page_,
+                            &access_, 1) != CUDA_SUCCESS) {
+          *err = "cuMemSetAccess failed";
+          driver_s_ += secs(t0);
+          return false;
+        }
+        run = i + 1;
       }
     }
-    if (wait && !lru_.empty()) {
-      Big* b = lru_.front();
-      if (b->ev) cudaEventSynchronize(b->ev);
-      evict(b);
-      return true;
-    }
-    return false;
+    driver_s_ += secs(t0);
+    return true;
   }
 
   void teardown() {
     if (!base_) return;
-    while (!lru_.empty()) evict(lru_.front());
-    for (auto& kv : live_) {
-      for (size_t i = 0; i < kv.second->pages; ++i)
-        drv_.unmap(reinterpret_cast<CUdeviceptr>(kv.first + i * page_), page_);
-      delete kv.second;
-    }
-    for (size_t p = 0; p < small_pages_.size(); ++p)
-      if (small_pages_[p] >= 0) drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
-    for (auto h : handles_)
-      if (h) drv_.release(h);
+    for (size_t p = 0; p < handle_of_.size(); ++p)
+      if (handle_of_[p] >= 0) drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
+    for (auto h : handles_) drv_.release(h);
     drv_.address_free(reinterpret_cast<CUdeviceptr>(base_), small_va_ + large_va_);
     base_ = nullptr;
   }
@@ -413,25 +374,17 @@ class VmmPool {
   Drv drv_;
   CUmemAllocationProp prop_{};
   CUmemAccessDesc access_{};
+  void* fresh_ = nullptr;
   size_t page_ = size_t(2) << 20;
   size_t small_va_ = 0, large_va_ = 0;
   char* base_ = nullptr;
-
-  Arena small_;                          // small blocks over the first region
-  std::vector<int32_t> small_pages_;     // small-region page -> handle (-1 unmapped)
-  std::vector<uint32_t> small_live_;     // small-region page -> live blocks
-  size_t small_mapped_ = 0, small_bytes_ = 0;
-
-  Arena va_;                             // unmapped VA of the large region
-  std::map<char*, Big*> live_;           // live large blocks by address
-  std::multimap<size_t, Big*> cache_;    // pages -> cached (free, mapped) block
-  std::list<Big*> lru_;                  // cached blocks, least recently freed first
-  size_t big_mapped_ = 0, big_live_pages_ = 0, big_bytes_ = 0;
-
+  Arena small_, large_;
+  std::vector<int32_t> handle_of_;   // VA page -> physical page (-1: unmapped)
+  std::vector<uint32_t> live_;       // VA page -> live blocks touching it
   std::vector<CUmemGenericAllocationHandle> handles_;
-  std::vector<int> free_;                // created, unmapped pages
-  size_t created_ = 0, limit_pages_ = 0;
-  uint64_t n_map_ = 0, n_unmap_ = 0, n_hits_ = 0;
+  std::vector<int> free_;            // physical pages not mapped anywhere
+  size_t created_ = 0, limit_pages_ = 0, mapped_ = 0, bytes_live_ = 0, live_pages_ = 0;
+  uint64_t n_map_ = 0, n_unmap_ = 0, n_moves_ = 0;
   double driver_s_ = 0;
 };
 

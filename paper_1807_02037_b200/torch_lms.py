@@ -276,6 +276,7 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
 
     saved_tensor_id = {}
     seen_edge = set()
+    self_prod = {}  # saved index -> op that produced a grad_fn-less tensor (its first saver)
     for k, si in enumerate(pack_saved):
         if si < 0:
             continue
@@ -283,7 +284,7 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
         cons = cap.consumer[k]
         if s.producer is None:
             continue  # params and inputs stay resident (variables are never swapped)
-        prod = cons if s.producer == "self" else s.producer
+        prod = self_prod.setdefault(si, cons) if s.producer == "self" else s.producer
         if s.producer != "self" and s.nbytes == 0:
             continue
         tid = saved_tensor_id.get(si)
