@@ -50,6 +50,7 @@ class Arena {
     b->off = 0;
     b->size = cap_;
     b->tag = fresh_;
+    b->owner = this;
     head_ = b;
     free_.insert({b->size, b});
   }
@@ -88,6 +89,7 @@ class Arena {
       rest->size = pick->size - size;
       rest->tag = pick->tag;
       rest->seq = pick->seq;
+      rest->owner = this;
       rest->prev = pick;
       rest->next = pick->next;
       if (pick->next) pick->next->prev = rest;
