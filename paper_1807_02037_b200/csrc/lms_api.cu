@@ -288,17 +288,15 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
   if (rc) return rc;
   VmmPool& v = *c->vmm;
   reap_deferred(c, false);
-  const size_t page = v.page();
-  const size_t want = (Arena::round(size) + page - 1) / page;
-  const size_t limit_pages = c->limit / page;
-  const size_t deferred_pages = (c->deferred_bytes + page - 1) / page;
-  const size_t live = v.live_pages();
-  // the non-deferred live set only shrinks by frees the caller has not made
-  // yet: fail at once (cuDNN's plan loop probes oversized workspaces)
-  if (live - std::min(live, deferred_pages) + want > limit_pages)
+  const size_t rsize = Arena::round(size);
+  // the budget is on live bytes; the non-deferred live set only shrinks by
+  // frees the caller has not made yet, so fail at once if it plus the request
+  // is over (cuDNN's plan loop probes oversized workspaces and expects a
+  // quick OOM); if deferred frees are in the way, wait for their copies
+  if (c->alloc_bytes - c->deferred_bytes + rsize > c->limit)
     return oom(c, size, "live set plus request exceeds the budget");
-  if (live + want > limit_pages) reap_deferred(c, true);
-  if (v.live_pages() + want > limit_pages) return oom(c, size, "live set plus request exceeds the budget");
+  if (c->alloc_bytes + rsize > c->limit) reap_deferred(c, true);
+  if (c->alloc_bytes + rsize > c->limit) return oom(c, size, "live set plus request exceeds the budget");
   std::string err;
   Block* b = v.alloc(size, stream, false, &err);
   if (!b && !c->deferred.empty()) {

@@ -1,10 +1,13 @@
 // Device pool over CUDA virtual memory: the budget caps PHYSICAL pages.
 //
-// The budget's worth of physical pages (the driver's allocation granularity,
-// 2 MiB on B200) is created and mapped once, contiguously, at the start of a
-// much larger reserved VA range.  Two best-fit arenas carve the VA: small
-// blocks (<= 1 MiB, 512 B granules, several per page) and large blocks
-// (page-aligned).  While the mapped region has a free range that fits, this
+// The budget's worth of physical pages is created and mapped once,
+// contiguously, at the start of a much larger reserved VA range.  Pages are
+// 64 MiB (a multiple of the driver's 2 MiB granularity): on B200 the cost of
+// cuMemSetAccess / cuMemUnmap is per mapped handle (~0.6 ms / ~0.2 ms for a
+// 2 MiB page, measured by scripts/micro/vmm_cost.cu), so large pages make a
+// page move ~16x cheaper per byte.  Two best-fit arenas carve the VA: small
+// blocks (<= 1 MiB, 512 B granules) and large blocks (2 MiB granules); blocks
+// share pages, and a page can move only when no live block touches it.  While the mapped region has a free range that fits, this
 // is an ordinary caching allocator: split and merge in place, no driver call.
 // Only when fragmentation leaves no mapped range large enough does the pool
 // move pages: it unmaps idle pages of free ranges and maps them under a free
@@ -139,7 +142,7 @@ class VmmPool {
 
   // reserve VA, create `limit_bytes` of pages and map them at the start of
   // the large region
-  bool init(int device, size_t limit_bytes, void* fresh, std::string* err) {
+  bool init(int device, size_t limit_bytes, void* fresh, std::string* err, size_t page_bytes = size_t(64) << 20) {
     if (!drv_.load(err)) return false;
     fresh_ = fresh;
     prop_ = CUmemAllocationProp{};
@@ -151,7 +154,8 @@ class VmmPool {
       *err = "cuMemGetAllocationGranularity failed";
       return false;
     }
-    page_ = g;
+    gran_ = g;
+    page_ = std::max(g, (page_bytes + g - 1) / g * g);
     limit_pages_ = limit_bytes / page_;
     small_va_ = size_t(8) << 30;
     large_va_ = std::max(4 * limit_pages_ * page_, size_t(64) << 30);
@@ -162,7 +166,7 @@ class VmmPool {
     }
     base_ = reinterpret_cast<char*>(base);
     small_.init(base_, small_va_, fresh, Arena::kAlign);
-    large_.init(base_ + small_va_, large_va_, fresh, page_);
+    large_.init(base_ + small_va_, large_va_, fresh, gran_);
     handle_of_.assign((small_va_ + large_va_) / page_, -1);
     live_.assign(handle_of_.size(), 0);
     access_.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -375,7 +379,7 @@ class VmmPool {
   CUmemAllocationProp prop_{};
   CUmemAccessDesc access_{};
   void* fresh_ = nullptr;
-  size_t page_ = size_t(2) << 20;
+  size_t page_ = size_t(64) << 20, gran_ = size_t(2) << 20;
   size_t small_va_ = 0, large_va_ = 0;
   char* base_ = nullptr;
   Arena small_, large_;
