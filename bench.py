@@ -343,8 +343,14 @@ def main():
             gc.collect()
             torch.cuda.synchronize(dev)
             ctx.synchronize()
+            n_live, top = ctx.live_blocks(6)
+            log(f"[bench]   after OOM cleanup: live {ctx.stats()['device_in_use'] / GIB:.2f} GiB in {n_live} blocks, "
+                f"largest {[round(b / MIB) for b in top]} MiB")
         return ok
 
+    torch.cuda.synchronize(dev)
+    ctx.synchronize()
+    log(f"[bench] before swapped runs: live {ctx.stats()['device_in_use'] / GIB:.2f} GiB")
     n_try = n_t if n_t < len(order) else -1
     fitted = try_swap(bs, n_try) or (n_try != -1 and try_swap(bs, -1))
     if not fitted:

@@ -158,6 +158,7 @@ class _Capture:
         key = (t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype)
         self.packs.append((key, t.numel() * t.element_size(), t.grad_fn, t.is_leaf,
                            t.requires_grad, isinstance(t, torch.nn.Parameter)))
+        t = t.detach()   # no tensor -> grad_fn -> saved -> tensor cycle (see SwapExecutor.pack)
         self.keep.append(t)
         return (k, t)
 
@@ -442,7 +443,11 @@ class SwapExecutor:
             k_counter[0] = k + 1
             si = plan.pack_saved[k] if k < plan.n_packs else -1
             if si < 0:
-                return t
+                # detached alias, not ``t``: an op output saved as itself would
+                # form a tensor -> grad_fn -> saved -> tensor cycle that only a
+                # completed backward breaks (a step that fails in forward would
+                # leak its activations)
+                return t.detach()
             h = handles.get(si)
             if h is None:
                 h = ctx.swap_out(t, self._codec_for(si, t), stream_of())

@@ -1,0 +1,10 @@
+#!/bin/bash
+# One GPU-box pass: GPU parity tests, smoke, then a bench line.  Logs land in gpurun_out/.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+nvidia-smi > gpurun_out/nvidia_smi.txt 2>&1
+nvidia-smi topo -m > gpurun_out/topo.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout ${BENCH_TIMEOUT:-1200} python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.log; echo "bench rc=$?" >> gpurun_out/bench.log
+tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -5 gpurun_out/bench.log; cat gpurun_out/bench.json
