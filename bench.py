@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--arch", default="resnet50")
     ap.add_argument("--budget-gib", type=float, default=16.0)
     ap.add_argument("--factor", type=float, default=4.7)
-    ap.add_argument("--codec", default="ce", choices=["ce", "sm", "zvc", "auto"])
+    ap.add_argument("--codec", default="auto", choices=["ce", "sm", "zvc", "auto"])
     ap.add_argument("--lb", type=int, default=1)
     ap.add_argument("--ub", type=int, default=10000)
     ap.add_argument("--strategy", default="chain_rule")
@@ -154,7 +154,10 @@ def measure_host_link(torch, dev, nbytes=512 * MIB):
 
 
 def is_oom(exc) -> bool:
-    return "LMS_OOM" in str(exc) or "out of memory" in str(exc).lower()
+    """Budget exhaustion, including cuDNN's report of a workspace it could not allocate."""
+    msg = str(exc)
+    return ("LMS_OOM" in msg or "out of memory" in msg.lower()
+            or "unable to find an engine" in msg or "CUDNN_STATUS_ALLOC_FAILED" in msg)
 
 
 def main():
@@ -288,7 +291,7 @@ def main():
     xc, yc = batch(cap_b)
     cfg0 = RewriteConfig(lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
                          fuse_swapins=args.fuse_swapins, swapin_fuse_distance=1)
-    codec = "ce" if args.codec == "auto" else args.codec
+    codec = args.codec
     lms = LMS(model, loss_fn, opt, cfg0, ctx, codec=codec, min_swap_bytes=(256 << 10) // cap_b)
     t_cap = time.perf_counter()
     plan = lms.capture(xc, yc)
@@ -307,9 +310,6 @@ def main():
     while n_t < len(order) and acc * bs < 1.15 * need:
         acc += order[n_t]
         n_t += 1
-    if args.codec == "auto":
-        codec_map = auto_codecs(lms)
-        lms._exec.codec = codec_map
     log(f"[bench] swap batch {bs}: {len(order)} candidate tensors, {sum(order) / MIB:.1f} MiB/img; "
         f"need {need / GIB:.2f} GiB off-device -> n_tensors={n_t}")
 
@@ -321,8 +321,6 @@ def main():
         cfg = RewriteConfig(n_tensors=n_tensors, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
                             fuse_swapins=args.fuse_swapins, swapin_fuse_distance=1)
         lms.replan(cfg)
-        if args.codec == "auto":
-            lms._exec.codec = codec_map
         xb, yb = batch(nb, seed=7)
         try:
             for _ in range(max(1, args.warmup)):
@@ -503,11 +501,6 @@ def timed(torch, dev, ws, fn, steps):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
     return ms
-
-
-def auto_codecs(lms):
-    """ZVC for tensors whose capture-time contents are mostly zero words, else copy engine."""
-    return "zvc"
 
 
 def run_reference(args, ws, rank):

@@ -111,6 +111,10 @@ int lms_set_home_stream(lms_ctx* ctx, void* stream);
 int lms_set_limit(lms_ctx* ctx, size_t limit);
 int lms_reset_peaks(lms_ctx* ctx);
 int lms_get_streams(lms_ctx* ctx, void** d2h, void** h2d);
+/* Tuning of the zero-copy kernels: CTAs per launch (0 = keep) and whether the
+ * ZVC kernels move chunks with bulk async copies (1, TMA path) or with
+ * per-thread 16 B loads/stores (0); -1 keeps the current setting. */
+int lms_set_tuning(lms_ctx* ctx, int zc_ctas, int use_bulk);
 
 /* ---- device pool (replaces the simulator's residency model) ------------- */
 int lms_dev_alloc(lms_ctx* ctx, size_t size, void* stream, void** out);

@@ -210,53 +210,116 @@ __global__ void copy_tail_kernel(char* __restrict__ dst, const char* __restrict_
 }
 
 // -------------------------------------------------------------------------
-// ZVC: lossless zero-value compression over 32-bit words.
+// Bulk asynchronous copies (the 1-D TMA path: cp.async.bulk, SASS UBLKCP)
+// and mbarriers.  Used by the ZVC kernels to move whole tile chunks between
+// shared memory and global memory -- HBM or mapped pinned host memory.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "ZVC_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra ZVC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global (HBM or mapped host) -> shared, completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// shared -> global (HBM or mapped host), tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N groups still reading their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// at most N groups not yet complete (writes performed)
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// generic-proxy shared-memory writes become visible to the async (bulk) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// -------------------------------------------------------------------------
+// ZVC: lossless zero-value compression over 32-bit words (stream format v2).
 //
-// Stream layout (all offsets in bytes from the start, 16B aligned):
-//   [0, 64)                 header  {magic, mode, nwords, ntiles, total_nnz, ...}
-//   [64, 64+4*T16)          per-tile value offsets (words), T16 = ntiles rounded to 4
-//   [.., +512*ntiles)       per-tile bitmask, 128 words per tile
-//   [.., +4*total_nnz)      packed nonzero words, tile order
-// A tile is 4096 words (16 KiB).  mode 1 = ZVC, mode 0 = raw fallback (the
-// words follow the header directly) chosen on device when compression would
-// not shrink the stream.
+// A swapped activation is compressed on its way out (SM kernels writing
+// straight into mapped pinned memory) and decompressed on its way in (SM
+// kernels reading straight out of pinned memory), so only the compressed
+// bytes cross the host link and no device staging buffer is needed.
+//
+// Stream layout (bytes from the start; every region 16 B aligned):
+//   [0, 64)                  header {magic "ZVC2", mode, nwords, ntiles, total_nnz, bytes, data_pos}
+//   [64, data_pos)           u32 chunk offsets, ntiles+1 entries, in 16 B units from data_pos
+//   [data_pos, bytes)        one chunk per tile, in tile order:
+//                              128-word bitmask (bit j of word s: word 32s+j of the tile is nonzero)
+//                              the tile's nonzero words in order, zero-padded to 16 B
+// A tile is 4096 words (16 KiB).  mode 0 = raw: the words follow the header
+// directly; the scan kernel picks it on the device when compression would
+// not shrink the stream.  Words past nwords in the last tile encode as zero.
 
 constexpr int kZvcTileWords = 4096;
-constexpr int kZvcMaskWords = kZvcTileWords / 32;  // 128
-constexpr uint32_t kZvcMagic = 0x5A564331u;          // "ZVC1"
+constexpr int kZvcMaskWords = kZvcTileWords / 32;                  // 128
+constexpr int kZvcChunkWords = kZvcMaskWords + kZvcTileWords;       // worst-case chunk (4224 words)
+constexpr int kZvcSmemBytes = 2 * kZvcChunkWords * 4;               // double-buffered chunks
+constexpr uint32_t kZvcMagic = 0x3243565Au;                          // "ZVC2"
 
 struct ZvcHeader {
   uint32_t magic, mode;
-  uint64_t nwords, ntiles, total_nnz, bytes;
-  uint64_t pad[3];
+  uint64_t nwords, ntiles, total_nnz, bytes, data_pos;
+  uint64_t pad[2];
 };
 static_assert(sizeof(ZvcHeader) == 64, "header is 64 bytes");
 
 __host__ __device__ inline uint64_t zvc_tiles(uint64_t nwords) {
   return (nwords + kZvcTileWords - 1) / kZvcTileWords;
 }
-__host__ __device__ inline uint64_t zvc_off_bytes(uint64_t ntiles) { return ((ntiles + 3) / 4) * 16; }
-__host__ __device__ inline uint64_t zvc_mask_pos(uint64_t ntiles) { return 64 + zvc_off_bytes(ntiles); }
-__host__ __device__ inline uint64_t zvc_vals_pos(uint64_t ntiles) {
-  return zvc_mask_pos(ntiles) + ntiles * kZvcMaskWords * 4;
-}
+__host__ __device__ inline uint64_t zvc_data_pos(uint64_t ntiles) { return 64 + ((ntiles + 1 + 3) / 4) * 16; }
+__host__ __device__ inline uint64_t zvc_raw_bytes(uint64_t nwords) { return 64 + (nwords * 4 + 15) / 16 * 16; }
 __host__ __device__ inline uint64_t zvc_bound(uint64_t nwords) {
-  uint64_t t = zvc_tiles(nwords);
-  uint64_t a = zvc_vals_pos(t) + nwords * 4;
-  uint64_t b = 64 + nwords * 4;
-  a = a > b ? a : b;
-  return (a + 15) / 16 * 16;
+  const uint64_t t = zvc_tiles(nwords);
+  const uint64_t a = zvc_data_pos(t) + t * uint64_t(kZvcChunkWords) * 4;  // every tile dense
+  const uint64_t b = zvc_raw_bytes(nwords);
+  return a > b ? a : b;
 }
 
-// pass 1: nonzero count per tile
+// pass 1: nonzero words per tile (HBM read; the source stays on the device)
 __global__ void __launch_bounds__(256) zvc_count_kernel(const uint32_t* __restrict__ src, uint64_t nwords,
                                                         uint32_t* __restrict__ counts) {
   __shared__ uint32_t red[8];
   const uint64_t ntiles = zvc_tiles(nwords);
+  const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const uint64_t base = t * kZvcTileWords;
     uint32_t c = 0;
-    if (base + kZvcTileWords <= nwords) {
+    if (vec && base + kZvcTileWords <= nwords) {
       const uint4* s4 = reinterpret_cast<const uint4*>(src + base);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -264,7 +327,8 @@ __global__ void __launch_bounds__(256) zvc_count_kernel(const uint32_t* __restri
         c += (v.x != 0) + (v.y != 0) + (v.z != 0) + (v.w != 0);
       }
     } else {
-      for (uint64_t i = base + threadIdx.x; i < nwords; i += 256) c += src[i] != 0;
+      const uint64_t end = base + kZvcTileWords < nwords ? base + kZvcTileWords : nwords;
+      for (uint64_t i = base + threadIdx.x; i < end; i += 256) c += src[i] != 0;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -279,18 +343,25 @@ __global__ void __launch_bounds__(256) zvc_count_kernel(const uint32_t* __restri
   }
 }
 
-// pass 2 (one CTA): exclusive scan of tile counts -> offsets, write header.
-// `offsets` is device scratch; the header and offsets also go to `out`.
+// pass 2 (one CTA): chunk sizes -> exclusive offsets; header and offset table
+// go to `out`; offsets[ntiles+1] carries the mode to the encode kernel.
 __global__ void __launch_bounds__(1024) zvc_scan_kernel(const uint32_t* __restrict__ counts, uint64_t nwords,
                                                         uint32_t* __restrict__ offsets, char* __restrict__ out) {
   __shared__ uint32_t warp_tot[32];
   __shared__ uint32_t carry;
+  __shared__ unsigned long long nnz_tot;
   const uint64_t ntiles = zvc_tiles(nwords);
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) {
+    carry = 0;
+    nnz_tot = 0;
+  }
   __syncthreads();
+  uint64_t my_nnz = 0;
   for (uint64_t base = 0; base < ntiles; base += 1024) {
-    uint64_t i = base + threadIdx.x;
-    uint32_t v = i < ntiles ? counts[i] : 0;
+    const uint64_t i = base + threadIdx.x;
+    const uint32_t nnz = i < ntiles ? counts[i] : 0;
+    my_nnz += nnz;
+    const uint32_t v = i < ntiles ? kZvcMaskWords / 4 + (nnz + 3) / 4 : 0;  // chunk size, 16 B units
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -309,169 +380,211 @@ __global__ void __launch_bounds__(1024) zvc_scan_kernel(const uint32_t* __restri
       warp_tot[threadIdx.x] = w;  // inclusive
     }
     __syncthreads();
-    uint32_t warp_base = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0;
-    uint32_t excl = carry + warp_base + x - v;
+    const uint32_t warp_base = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0;
+    const uint32_t excl = carry + warp_base + x - v;
     if (i < ntiles) offsets[i] = excl;
     __syncthreads();
     if (threadIdx.x == 1023) carry = excl + v;
     __syncthreads();
   }
+  atomicAdd(&nnz_tot, (unsigned long long)my_nnz);
+  __syncthreads();
+  uint32_t* table = reinterpret_cast<uint32_t*>(out + 64);
   if (threadIdx.x == 0) {
-    uint64_t total = carry;
     ZvcHeader h{};
     h.magic = kZvcMagic;
     h.nwords = nwords;
     h.ntiles = ntiles;
-    h.total_nnz = total;
-    uint64_t zbytes = zvc_vals_pos(ntiles) + total * 4;
-    uint64_t rbytes = 64 + nwords * 4;
+    h.total_nnz = nnz_tot;
+    h.data_pos = zvc_data_pos(ntiles);
+    const uint64_t zbytes = h.data_pos + uint64_t(carry) * 16;
+    const uint64_t rbytes = zvc_raw_bytes(nwords);
     h.mode = zbytes < rbytes ? 1u : 0u;
     h.bytes = h.mode ? zbytes : rbytes;
-    // the encode kernel reads the mode from the scratch copy
-    offsets[ntiles] = h.mode;
+    offsets[ntiles] = carry;
+    offsets[ntiles + 1] = h.mode;
     const uint4* hs = reinterpret_cast<const uint4*>(&h);
     uint4* ho = reinterpret_cast<uint4*>(out);
     for (int k = 0; k < 4; ++k) ho[k] = hs[k];
+    if (h.mode) table[ntiles] = carry;
   }
   __syncthreads();
-  // offsets table to the output (only meaningful in mode 1)
-  uint32_t* oo = reinterpret_cast<uint32_t*>(out + 64);
-  for (uint64_t i = threadIdx.x; i < ntiles; i += 1024) oo[i] = offsets[i];
+  if (offsets[ntiles + 1])
+    for (uint64_t i = threadIdx.x; i < ntiles; i += 1024) table[i] = offsets[i];
 }
 
-// pass 3: per tile, compact the nonzero words through shared memory and
-// write bitmask + values with 16B stores (or the raw words in mode 0).
+// raw mode body: 16 B words after the header (grid-stride), word tail by CTA 0
+__device__ __forceinline__ void zvc_raw_copy(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
+                                             uint64_t nwords) {
+  const uint64_t n16 = nwords / 4;
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  const uint64_t nth = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * nth < n16; i += 4 * nth) {
+    uint4 a = ld_stream(s4 + i), b = ld_stream(s4 + i + nth);
+    uint4 c = ld_stream(s4 + i + 2 * nth), e = ld_stream(s4 + i + 3 * nth);
+    st_stream(d4 + i, a); st_stream(d4 + i + nth, b);
+    st_stream(d4 + i + 2 * nth, c); st_stream(d4 + i + 3 * nth, e);
+  }
+  for (; i < n16; i += nth) st_stream(d4 + i, ld_stream(s4 + i));
+  if (blockIdx.x == 0)
+    for (uint64_t k = n16 * 4 + threadIdx.x; k < nwords; k += blockDim.x) dst[k] = src[k];
+}
+
+// exclusive scan of the 128 per-segment popcounts in seg[] (warp 0); seg[128] = total
+__device__ __forceinline__ void zvc_seg_scan(uint32_t* seg, int lane) {
+  uint32_t a = seg[lane * 4], b = seg[lane * 4 + 1], c = seg[lane * 4 + 2], e = seg[lane * 4 + 3];
+  uint32_t s = a + b + c + e, x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  const uint32_t ex = x - s;
+  seg[lane * 4] = ex;
+  seg[lane * 4 + 1] = ex + a;
+  seg[lane * 4 + 2] = ex + a + b;
+  seg[lane * 4 + 3] = ex + a + b + c;
+  if (lane == 31) seg[kZvcMaskWords] = x;
+}
+
+// pass 3: per tile, bitmask + compacted nonzeros assembled in shared memory,
+// then one bulk store of the whole chunk (TMA when use_bulk, else 16 B STG).
+// Double-buffered: tile k+1 is compacted while tile k's chunk is in flight.
 __global__ void __launch_bounds__(256) zvc_encode_kernel(const uint32_t* __restrict__ src, uint64_t nwords,
                                                          const uint32_t* __restrict__ offsets,
-                                                         char* __restrict__ out) {
-  __shared__ uint32_t vals[kZvcTileWords];
-  __shared__ uint32_t mask[kZvcMaskWords];
+                                                         char* __restrict__ out, int use_bulk) {
+  extern __shared__ __align__(128) uint32_t zsm[];
   __shared__ uint32_t seg[kZvcMaskWords + 1];
   const uint64_t ntiles = zvc_tiles(nwords);
-  const uint32_t mode = offsets[ntiles];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (mode == 0) {
-    // raw fallback: words after the header, 16B body + word tail
-    uint4* o4 = reinterpret_cast<uint4*>(out + 64);
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint64_t n16 = nwords / 4;
-    for (uint64_t i = uint64_t(blockIdx.x) * 256 + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * 256)
-      st_stream(o4 + i, ld_stream(s4 + i));
-    if (blockIdx.x == 0) {
-      uint32_t* ow = reinterpret_cast<uint32_t*>(out + 64);
-      for (uint64_t i = n16 * 4 + threadIdx.x; i < nwords; i += 256) ow[i] = src[i];
-    }
+  if (offsets[ntiles + 1] == 0) {  // raw mode
+    zvc_raw_copy(reinterpret_cast<uint32_t*>(out + 64), src, nwords);
     return;
   }
-  uint32_t* mask_out = reinterpret_cast<uint32_t*>(out + zvc_mask_pos(ntiles));
-  uint32_t* vals_out = reinterpret_cast<uint32_t*>(out + zvc_vals_pos(ntiles));
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  char* data = out + zvc_data_pos(ntiles);
+  int buf = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
+    uint32_t* chunk = zsm + buf * kZvcChunkWords;
+    if (use_bulk && threadIdx.x == 0) bulk_wait_read<1>();  // the store that last read this buffer
+    __syncthreads();
     const uint64_t base = t * kZvcTileWords;
-    // round r covers words [r*256, r*256+256); warp w of round r is segment r*8+w
     uint32_t w16[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      uint64_t i = base + r * 256 + threadIdx.x;
+      const uint64_t i = base + r * 256 + threadIdx.x;
       w16[r] = i < nwords ? __ldg(src + i) : 0u;
-      uint32_t m = __ballot_sync(0xffffffffu, w16[r] != 0);
-      if (lane == 0) { mask[r * 8 + warp] = m; seg[r * 8 + warp] = __popc(m); }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t m = __ballot_sync(0xffffffffu, w16[r] != 0);
+      if (lane == 0) {
+        chunk[r * 8 + warp] = m;
+        seg[r * 8 + warp] = __popc(m);
+      }
     }
     __syncthreads();
-    if (warp == 0) {  // exclusive scan over the 128 segment counts
-      uint32_t a = seg[lane * 4], b = seg[lane * 4 + 1], c = seg[lane * 4 + 2], e = seg[lane * 4 + 3];
-      uint32_t s = a + b + c + e, x = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      uint32_t ex = x - s;
-      seg[lane * 4] = ex; seg[lane * 4 + 1] = ex + a; seg[lane * 4 + 2] = ex + a + b;
-      seg[lane * 4 + 3] = ex + a + b + c;
-      if (lane == 31) seg[kZvcMaskWords] = x;
-    }
+    if (warp == 0) zvc_seg_scan(seg, lane);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      uint32_t m = mask[r * 8 + warp];
-      if (w16[r] != 0) vals[seg[r * 8 + warp] + __popc(m & ((1u << lane) - 1u))] = w16[r];
+      const uint32_t m = chunk[r * 8 + warp];
+      if (w16[r] != 0) chunk[kZvcMaskWords + seg[r * 8 + warp] + __popc(m & ((1u << lane) - 1u))] = w16[r];
     }
-    __syncthreads();
-    // bitmask: 128 words = 32 x 16B
-    if (threadIdx.x < 32)
-      st_stream(reinterpret_cast<uint4*>(mask_out + t * kZvcMaskWords) + threadIdx.x,
-                reinterpret_cast<const uint4*>(mask)[threadIdx.x]);
-    // values: head words until 16B aligned, 16B body, tail words
     const uint32_t n = seg[kZvcMaskWords];
-    const uint64_t o = offsets[t];
-    uint32_t* dstw = vals_out + o;
-    uint32_t head = (uint32_t)((4 - (o & 3)) & 3);
-    if (head > n) head = n;
-    if (threadIdx.x < head) dstw[threadIdx.x] = vals[threadIdx.x];
-    const uint32_t body16 = (n - head) / 4;
-    // shared-memory source is only 4B aligned after `head` words: assemble in registers
-    for (uint32_t k = threadIdx.x; k < body16; k += 256) {
-      const uint32_t* sv = vals + head + 4 * k;
-      st_stream(reinterpret_cast<uint4*>(dstw + head) + k, make_uint4(sv[0], sv[1], sv[2], sv[3]));
+    const uint32_t padded = (n + 3) & ~3u;
+    if (threadIdx.x < padded - n) chunk[kZvcMaskWords + n + threadIdx.x] = 0u;
+    const uint32_t bytes = (kZvcMaskWords + padded) * 4;
+    char* dst = data + uint64_t(offsets[t]) * 16;
+    if (use_bulk) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        bulk_s2g(dst, chunk, bytes);
+        bulk_commit();
+      }
+    } else {
+      __syncthreads();
+      const uint4* c4 = reinterpret_cast<const uint4*>(chunk);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      for (uint32_t k = threadIdx.x; k < bytes / 16; k += 256) st_stream(d4 + k, c4[k]);
     }
-    for (uint32_t k = head + body16 * 4 + threadIdx.x; k < n; k += 256) dstw[k] = vals[k];
-    __syncthreads();
   }
+  if (use_bulk && threadIdx.x == 0) bulk_wait<0>();
 }
 
-// decode: `enc` is the whole stream already in HBM (H2D-staged).
+// decode: `enc` may live in HBM or in mapped pinned host memory (zero-copy
+// swap-in).  Each CTA walks its tiles with a two-deep pipeline: the bulk
+// load of tile k+1's chunk is in flight while tile k is expanded from shared
+// memory into coalesced HBM stores.
 __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict__ enc, uint64_t nwords,
-                                                         uint32_t* __restrict__ dst) {
-  __shared__ uint32_t mask[kZvcMaskWords];
-  __shared__ uint32_t seg[kZvcMaskWords];
+                                                         uint32_t* __restrict__ dst, int use_bulk) {
+  extern __shared__ __align__(128) uint32_t zsm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ uint32_t seg[kZvcMaskWords + 1];
+  __shared__ uint32_t s_mode;
   const ZvcHeader* h = reinterpret_cast<const ZvcHeader*>(enc);
-  const uint64_t ntiles = zvc_tiles(nwords);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (h->mode == 0) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(enc + 64);
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-    uint64_t n16 = nwords / 4;
-    for (uint64_t i = uint64_t(blockIdx.x) * 256 + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * 256)
-      d4[i] = ld_stream(s4 + i);
-    if (blockIdx.x == 0) {
-      const uint32_t* sw = reinterpret_cast<const uint32_t*>(enc + 64);
-      for (uint64_t i = n16 * 4 + threadIdx.x; i < nwords; i += 256) dst[i] = sw[i];
-    }
+  if (threadIdx.x == 0) s_mode = h->mode;
+  __syncthreads();
+  if (s_mode == 0) {
+    zvc_raw_copy(dst, reinterpret_cast<const uint32_t*>(enc + 64), nwords);
     return;
   }
+  const uint64_t ntiles = zvc_tiles(nwords);
   const uint32_t* offs = reinterpret_cast<const uint32_t*>(enc + 64);
-  const uint32_t* mask_in = reinterpret_cast<const uint32_t*>(enc + zvc_mask_pos(ntiles));
-  const uint32_t* vals_in = reinterpret_cast<const uint32_t*>(enc + zvc_vals_pos(ntiles));
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    if (threadIdx.x < kZvcMaskWords) {
-      uint32_t m = mask_in[t * kZvcMaskWords + threadIdx.x];
-      mask[threadIdx.x] = m;
-      seg[threadIdx.x] = __popc(m);
+  const char* data = enc + zvc_data_pos(ntiles);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (use_bulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      fence_mbar_init();
     }
     __syncthreads();
-    if (warp == 0) {
-      uint32_t a = seg[lane * 4], b = seg[lane * 4 + 1], c = seg[lane * 4 + 2], e = seg[lane * 4 + 3];
-      uint32_t s = a + b + c + e, x = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+  }
+  auto issue = [&](uint64_t t, int b) {  // thread 0 only
+    const uint32_t a = offs[t], e = offs[t + 1];
+    const uint32_t bytes = (e - a) * 16;
+    mbar_expect_tx(&bar[b], bytes);
+    bulk_g2s(zsm + b * kZvcChunkWords, data + uint64_t(a) * 16, bytes, &bar[b]);
+  };
+  uint32_t phase0 = 0, phase1 = 0;
+  if (use_bulk && threadIdx.x == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  int b = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, b ^= 1) {
+    uint32_t* chunk = zsm + b * kZvcChunkWords;
+    if (use_bulk) {
+      const uint64_t tn = t + gridDim.x;
+      if (threadIdx.x == 0 && tn < ntiles) issue(tn, b ^ 1);
+      if (b == 0) {
+        mbar_wait(&bar[0], phase0);
+        phase0 ^= 1;
+      } else {
+        mbar_wait(&bar[1], phase1);
+        phase1 ^= 1;
       }
-      uint32_t ex = x - s;
-      seg[lane * 4] = ex; seg[lane * 4 + 1] = ex + a; seg[lane * 4 + 2] = ex + a + b;
-      seg[lane * 4 + 3] = ex + a + b + c;
+    } else {
+      const uint32_t a = offs[t], e = offs[t + 1];
+      const uint4* s4 = reinterpret_cast<const uint4*>(data + uint64_t(a) * 16);
+      uint4* c4 = reinterpret_cast<uint4*>(chunk);
+      for (uint32_t k = threadIdx.x; k < e - a; k += 256) c4[k] = ld_stream(s4 + k);
+      __syncthreads();
     }
+    if (threadIdx.x < kZvcMaskWords) seg[threadIdx.x] = __popc(chunk[threadIdx.x]);
     __syncthreads();
-    const uint32_t* tv = vals_in + offs[t];
+    if (warp == 0) zvc_seg_scan(seg, lane);
+    __syncthreads();
     const uint64_t base = t * kZvcTileWords;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      uint64_t i = base + r * 256 + threadIdx.x;
-      uint32_t m = mask[r * 8 + warp];
-      uint32_t v = ((m >> lane) & 1u) ? tv[seg[r * 8 + warp] + __popc(m & ((1u << lane) - 1u))] : 0u;
+      const uint64_t i = base + r * 256 + threadIdx.x;
+      const uint32_t m = chunk[r * 8 + warp];
+      const uint32_t v =
+          ((m >> lane) & 1u) ? chunk[kZvcMaskWords + seg[r * 8 + warp] + __popc(m & ((1u << lane) - 1u))] : 0u;
       if (i < nwords) dst[i] = v;
     }
-    __syncthreads();
+    __syncthreads();  // chunk buffer b is free for the load issued two tiles from now
   }
 }
 

@@ -129,6 +129,9 @@ struct lms_handle {
   bool wire_known = true;          // false until a ZVC header has been read back
   int64_t rec_out = -1;            // index of the swap-out timing record
   int64_t rec_in = -1;             // index of the last swap-in timing record
+  uint64_t rec_gen = 0;            // trace generation the record indices belong to
+  std::vector<int64_t> zvc_in_recs;  // ZVC swap-in records issued before the size was known
+  uint64_t zvc_in_pending = 0;       // such swap-ins not yet in the h2d wire counter
   bool released = false;
 };
 
@@ -173,6 +176,9 @@ struct lms_ctx {
   // timing
   cudaEvent_t epoch = nullptr;
   std::vector<XferRec> recs;
+  uint64_t trace_gen = 0;   // bumped by lms_trace_clear
+  int use_bulk = 1;         // ZVC kernels move chunks with cp.async.bulk (LMS_ZVC_BULK=0: STG/LDG)
+  int zc_ctas = 0;          // CTAs of the zero-copy (host-side) kernels
   // consumer reached its wait (event on the consumer stream) vs swap-in record
   std::vector<std::pair<cudaEvent_t, int64_t>> waits;
 };
@@ -408,7 +414,14 @@ void account_zvc(lms_ctx* c) {
     h->wire = hd->magic == kZvcMagic ? hd->bytes : h->host_bytes;
     h->wire_known = true;
     c->st.d2h_wire_bytes += h->wire;
-    if (h->rec_out >= 0 && size_t(h->rec_out) < c->recs.size()) c->recs[h->rec_out].wire = h->wire;
+    c->st.h2d_wire_bytes += h->wire * h->zvc_in_pending;
+    h->zvc_in_pending = 0;
+    if (h->rec_gen == c->trace_gen) {
+      if (h->rec_out >= 0 && size_t(h->rec_out) < c->recs.size()) c->recs[h->rec_out].wire = h->wire;
+      for (int64_t r : h->zvc_in_recs)
+        if (r >= 0 && size_t(r) < c->recs.size()) c->recs[r].wire = h->wire;
+    }
+    h->zvc_in_recs.clear();
   }
   c->zvc_open.resize(w);
 }
@@ -561,6 +574,15 @@ int launch_copy(lms_ctx* c, char* dst, const char* src, size_t bytes, cudaStream
   return LMS_OK;
 }
 
+bool is_host_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int ensure_zvc_scratch(lms_ctx* c, size_t words) {
   if (words <= c->zvc_scratch_words) return LMS_OK;
   if (c->zvc_scratch) {
@@ -574,24 +596,31 @@ int ensure_zvc_scratch(lms_ctx* c, size_t words) {
   return LMS_OK;
 }
 
-int launch_zvc_encode(lms_ctx* c, const uint32_t* src, uint64_t nwords, char* out, cudaStream_t s) {
-  uint64_t ntiles = zvc_tiles(nwords);
-  int rc = ensure_zvc_scratch(c, 2 * (ntiles + 1));
+int launch_zvc_encode(lms_ctx* c, const uint32_t* src, uint64_t nwords, char* out, cudaStream_t s,
+                      bool to_host) {
+  const uint64_t ntiles = zvc_tiles(nwords);
+  int rc = ensure_zvc_scratch(c, 2 * ntiles + 2);
   if (rc) return rc;
   uint32_t* counts = c->zvc_scratch;
-  uint32_t* offsets = c->zvc_scratch + ntiles + 1;
-  int grid = sm_grid(c, int64_t(ntiles), 1);
-  zvc_count_kernel<<<grid, 256, 0, s>>>(src, nwords, counts);
+  uint32_t* offsets = c->zvc_scratch + ntiles;
+  // pass 1 reads HBM only: the whole GPU; pass 3 writes the host link (or
+  // HBM): enough CTAs to keep the link busy without crowding the compute stream
+  const int grid_count = sm_grid(c, int64_t(ntiles), 1);
+  int grid_enc = grid_count;
+  if (to_host) grid_enc = int(std::min<int64_t>(int64_t(ntiles), c->zc_ctas));
+  zvc_count_kernel<<<grid_count, 256, 0, s>>>(src, nwords, counts);
   zvc_scan_kernel<<<1, 1024, 0, s>>>(counts, nwords, offsets, out);
-  zvc_encode_kernel<<<grid, 256, 0, s>>>(src, nwords, offsets, out);
+  zvc_encode_kernel<<<std::max(grid_enc, 1), 256, kZvcSmemBytes, s>>>(src, nwords, offsets, out, c->use_bulk);
   c->st.kernel_launches += 3;
   CK(cudaGetLastError());
   return LMS_OK;
 }
 
-int launch_zvc_decode(lms_ctx* c, const char* enc, uint64_t nwords, uint32_t* dst, cudaStream_t s) {
+int launch_zvc_decode(lms_ctx* c, const char* enc, uint64_t nwords, uint32_t* dst, cudaStream_t s,
+                      bool from_host) {
   int grid = sm_grid(c, int64_t(zvc_tiles(nwords)), 1);
-  zvc_decode_kernel<<<grid, 256, 0, s>>>(enc, nwords, dst);
+  if (from_host) grid = int(std::min<int64_t>(int64_t(zvc_tiles(nwords)), c->zc_ctas));
+  zvc_decode_kernel<<<std::max(grid, 1), 256, kZvcSmemBytes, s>>>(enc, nwords, dst, c->use_bulk);
   c->st.kernel_launches++;
   CK(cudaGetLastError());
   return LMS_OK;
@@ -642,6 +671,13 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
     return fail(LMS_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  // zero-copy kernels: one CTA per SM by default (each keeps a 16 KiB chunk
+  // in flight on the link), overridable for tuning
+  c->zc_ctas = cfg->sm_ctas > 0 ? cfg->sm_ctas : c->num_sms;
+  if (const char* v = getenv("LMS_ZC_CTAS")) c->zc_ctas = std::max(1, atoi(v));
+  if (const char* v = getenv("LMS_ZVC_BULK")) c->use_bulk = atoi(v) != 0;
+  cudaFuncSetAttribute(zvc_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
+  cudaFuncSetAttribute(zvc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   // transfers get the higher priority so their small kernels are not starved
@@ -730,6 +766,14 @@ int lms_reset_peaks(lms_ctx* c) {
   c->alloc_peak = c->alloc_bytes;
   c->mapped_peak = c->vmm ? c->vmm->mapped_bytes() : 0;
   c->host_peak = c->host_used;
+  return LMS_OK;
+}
+
+int lms_set_tuning(lms_ctx* c, int zc_ctas, int use_bulk) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  if (zc_ctas > 0) c->zc_ctas = zc_ctas;
+  if (use_bulk >= 0) c->use_bulk = use_bulk != 0;
   return LMS_OK;
 }
 
@@ -827,7 +871,7 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
         rc = launch_copy(c, h->host, static_cast<const char*>(src), stored, s);
       h->wire = stored;
     } else {
-      rc = launch_zvc_encode(c, static_cast<const uint32_t*>(src), stored / 4, h->host, s);
+      rc = launch_zvc_encode(c, static_cast<const uint32_t*>(src), stored / 4, h->host, s, true);
       h->wire = h->host_bytes;  // upper bound until the header is readable
     }
     if (rc) {
@@ -840,7 +884,10 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
   h->out_done->e = c->events.get();
   h->out_done->refs = 1;
   CK(cudaEventRecord(h->out_done->e, s));
-  if (c->cfg.timing && t0) h->rec_out = int64_t(c->recs.size());
+  if (c->cfg.timing && t0) {
+    h->rec_out = int64_t(c->recs.size());
+    h->rec_gen = c->trace_gen;
+  }
   timing_end(c, s, t0, h, 0, h->logical, h->wire);
   if (codec == LMS_CODEC_ZVC && stored) {
     h->wire_known = false;
@@ -904,17 +951,11 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
       rc = launch_layout<false>(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
       wire = stored;
     } else if (h->codec == LMS_CODEC_ZVC) {
-      uint64_t bytes = h->wire_known ? h->wire : h->host_bytes;
-      void* stage = nullptr;
-      rc = dev_alloc_locked(c, bytes, s, &stage);
-      if (rc == LMS_OK) {
-        CK(cudaMemcpyAsync(stage, h->host, bytes, cudaMemcpyHostToDevice, s));
-        rc = launch_zvc_decode(c, static_cast<char*>(stage), stored / 4, static_cast<uint32_t*>(dst), s);
-        dev_free_locked(c, stage, s);
-      } else {
-        return rc;  // no room for the staging copy under the budget
-      }
-      wire = bytes;
+      // zero-copy: the decode kernel reads the compressed stream straight out
+      // of pinned memory, so only the compressed bytes cross the link and no
+      // device staging buffer is taken from the budget
+      rc = launch_zvc_decode(c, h->host, stored / 4, static_cast<uint32_t*>(dst), s, true);
+      wire = h->wire_known ? h->wire : 0;
     } else if (h->codec == LMS_CODEC_RAW_SM && reinterpret_cast<uintptr_t>(dst) % 16 == 0) {
       rc = launch_copy(c, static_cast<char*>(dst), h->host, stored, s);
       wire = stored;
@@ -926,11 +967,21 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
   if (rc) return rc;
   if (!h->in_ready) h->in_ready = c->events.get();
   CK(cudaEventRecord(h->in_ready, s));
-  if (c->cfg.timing && t0) h->rec_in = int64_t(c->recs.size());
+  if (c->cfg.timing && t0) {
+    h->rec_in = int64_t(c->recs.size());
+    if (h->codec == LMS_CODEC_ZVC && !h->wire_known) {
+      if (h->rec_gen != c->trace_gen) h->zvc_in_recs.clear();
+      h->zvc_in_recs.push_back(h->rec_in);
+    }
+    h->rec_gen = c->trace_gen;
+  }
   timing_end(c, s, t0, h, 1, h->logical, wire);
   c->st.n_swap_in++;
   c->st.h2d_logical_bytes += h->logical;
-  c->st.h2d_wire_bytes += wire;
+  if (h->codec == LMS_CODEC_ZVC && !h->wire_known)
+    h->zvc_in_pending++;  // counted when the swap-out's header is readable
+  else
+    c->st.h2d_wire_bytes += wire;
   return LMS_OK;
 }
 
@@ -1025,14 +1076,14 @@ int lms_zvc_encode(lms_ctx* c, const void* src, size_t nwords, void* dst, void* 
     return fail(LMS_E_INVALID, "zvc buffers must be 16-byte aligned");
   std::lock_guard<std::mutex> g(c->mu);
   return launch_zvc_encode(c, static_cast<const uint32_t*>(src), nwords, static_cast<char*>(dst),
-                           static_cast<cudaStream_t>(stream));
+                           static_cast<cudaStream_t>(stream), is_host_ptr(dst));
 }
 
 int lms_zvc_decode(lms_ctx* c, const void* enc, size_t nwords, void* dst, void* stream) {
   if (!c || !enc || (!dst && nwords)) return fail(LMS_E_INVALID, "null argument");
   if (nwords == 0) return LMS_OK;
   return launch_zvc_decode(c, static_cast<const char*>(enc), nwords, static_cast<uint32_t*>(dst),
-                           static_cast<cudaStream_t>(stream));
+                           static_cast<cudaStream_t>(stream), is_host_ptr(enc));
 }
 
 int lms_zvc_encoded_size(const void* enc_host, size_t* out) {
@@ -1129,6 +1180,7 @@ int lms_trace_clear(lms_ctx* c) {
     c->events.put(r.end, true);
   }
   c->recs.clear();
+  c->trace_gen++;
   for (auto& w : c->waits) c->events.put(w.first, true);
   c->waits.clear();
   cudaEventRecord(c->epoch, c->d2h);

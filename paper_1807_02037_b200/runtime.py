@@ -81,6 +81,7 @@ def lib():
         "lms_set_global": ([vp], i), "lms_get_global": ([], vp),
         "lms_set_home_stream": ([vp, vp], i), "lms_set_limit": ([vp, sz], i),
         "lms_reset_peaks": ([vp], i), "lms_get_streams": ([vp, pp, pp], i),
+        "lms_set_tuning": ([vp, i, i], i),
         "lms_dev_alloc": ([vp, sz, vp, pp], i), "lms_dev_free": ([vp, vp, vp], i),
         "lms_dev_hold_until": ([vp, vp, vp], i),
         "lms_host_alloc": ([vp, sz, pp], i), "lms_host_free": ([vp, vp], i),
@@ -174,6 +175,10 @@ class Context:
 
     def set_limit(self, nbytes: int):
         _check(lib().lms_set_limit(self.ptr, nbytes), "lms_set_limit")
+
+    def set_tuning(self, zc_ctas: int = 0, use_bulk: int = -1):
+        """CTAs of the zero-copy kernels (0 = keep) and bulk-copy (TMA) use for ZVC (-1 = keep)."""
+        _check(lib().lms_set_tuning(self.ptr, zc_ctas, use_bulk), "lms_set_tuning")
 
     def reset_peaks(self):
         _check(lib().lms_reset_peaks(self.ptr), "lms_reset_peaks")

@@ -90,6 +90,7 @@ class _Saved:
     producer: object            # autograd node, "self" (saved by its own op) or None (leaf)
     is_param: bool
     packs: list = field(default_factory=list)   # pack indices that saved it
+    zero_frac: float = 0.0
 
 
 @dataclass
@@ -143,6 +144,7 @@ class _SavedInfo:
     tid: int
     nbytes: int
     swapped: bool
+    zero_frac: float = 0.0
 
 
 class _Capture:
@@ -152,12 +154,18 @@ class _Capture:
         self.packs = []        # pack idx -> (tensor key, nbytes, grad_fn or None, is_leaf, requires_grad)
         self.keep = []         # strong refs so addresses stay unique during capture
         self.consumer = {}     # pack idx -> autograd node that unpacked it
+        self.zero_frac = []    # pack idx -> share of zero words (capture-time contents)
 
     def pack(self, t):
         k = len(self.packs)
         key = (t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype)
         self.packs.append((key, t.numel() * t.element_size(), t.grad_fn, t.is_leaf,
                            t.requires_grad, isinstance(t, torch.nn.Parameter)))
+        # share of all-zero 32-bit words: what the ZVC codec would drop
+        zf = 0.0
+        if t.numel() and t.element_size() == 4 and not isinstance(t, torch.nn.Parameter):
+            zf = float((t.detach().view(torch.int32) == 0).sum()) / t.numel()
+        self.zero_frac.append(zf)
         t = t.detach()   # no tensor -> grad_fn -> saved -> tensor cycle (see SwapExecutor.pack)
         self.keep.append(t)
         return (k, t)
@@ -252,7 +260,7 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
                 producer = grad_fn
             else:
                 producer = "self"  # non-differentiable output of the saving op
-            s = _Saved(len(saved), nbytes, producer, is_param)
+            s = _Saved(len(saved), nbytes, producer, is_param, zero_frac=cap.zero_frac[k])
             by_key[key] = s
             saved.append(s)
         s.packs.append(k)
@@ -336,8 +344,8 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int)
     F = meta["F"]
     swapped_tids = {tid for _, _, tid in rep.edges_rewritten}
     pack_saved = meta["pack_saved"]
-    saved_info = [_SavedInfo(s.tid, s.nbytes, meta["saved_tensor_id"].get(s.tid) in swapped_tids)
-                  for s in meta["saved"]]
+    saved_info = [_SavedInfo(s.tid, s.nbytes, meta["saved_tensor_id"].get(s.tid) in swapped_tids,
+                             s.zero_frac) for s in meta["saved"]]
 
     # swap-in nodes -> groups
     groups = []
@@ -412,7 +420,13 @@ class SwapExecutor:
         self.codec = codec
         self.last_stats = {}
 
+    # ZVC pays off once enough words are zero: its stream is 1/32 bitmask
+    # plus the nonzero words, and it runs on SMs instead of the copy engine
+    ZVC_MIN_ZERO_FRAC = 0.25
+
     def _codec_for(self, si: int, t) -> str:
+        if self.codec == "auto":
+            return "zvc" if self.plan.saved[si].zero_frac >= self.ZVC_MIN_ZERO_FRAC else "ce"
         if isinstance(self.codec, str):
             return self.codec
         return self.codec.get(si, "ce")

@@ -55,10 +55,12 @@ def test_unpack_matches_copy(lms_ctx, dtype):
         assert torch.equal(dst, src), name
 
 
+@pytest.mark.parametrize("bulk", [1, 0])
 @pytest.mark.parametrize("nwords,density", [(0, 0.5), (1, 1.0), (3, 0.0), (4095, 0.5), (4096, 0.5),
                                             (4097, 0.3), (1 << 20, 0.5), (1 << 20, 0.0),
                                             (1 << 20, 1.0), ((1 << 22) + 13, 0.47)])
-def test_zvc_roundtrip(lms_ctx, nwords, density):
+def test_zvc_roundtrip(lms_ctx, nwords, density, bulk):
+    lms_ctx.set_tuning(0, bulk)
     torch.manual_seed(nwords)
     x = torch.randn(nwords, device="cuda")
     x = torch.where(torch.rand(nwords, device="cuda") < density, x, torch.zeros_like(x))
@@ -76,3 +78,4 @@ def test_zvc_roundtrip(lms_ctx, nwords, density):
     nnz = int((x.view(torch.int32) != 0).sum())
     if nwords:
         assert int(hdr[3]) == nnz  # total_nnz field
+    lms_ctx.set_tuning(0, 1)

@@ -104,3 +104,26 @@ def test_stats_count_bytes_and_kernels(lms_ctx):
     tr = lms_ctx.trace()
     assert {r["direction"] for r in tr} == {0, 1}
     assert all(r["end_ms"] >= r["start_ms"] for r in tr)
+
+
+@pytest.mark.parametrize("bulk,ctas", [(1, 0), (0, 0), (1, 3), (0, 5), (1, 1000)])
+def test_zvc_zero_copy_paths(lms_ctx, bulk, ctas):
+    """Encode into / decode out of pinned memory with bulk (TMA) and per-thread
+    copies, few and many CTAs: bit-exact, including ragged last tiles."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    lms_ctx.set_tuning(ctas or sms, bulk)
+    try:
+        g = torch.Generator(device="cuda").manual_seed(ctas + bulk)
+        for n in (1, 4095, 4096, 4097, 3 * 4096 + 5, (1 << 21) + 17):
+            x = torch.relu(torch.randn(n, device="cuda", generator=g))
+            x[: min(n, 7)] = torch.tensor([-0.0, float("nan"), 1.0, 0.0, -1.0, 0.0, 2.0], device="cuda")[: min(n, 7)]
+            h = lms_ctx.swap_out(x, "zvc")
+            outs = [lms_ctx.swap_in(h) for _ in range(2)]  # two swap-ins of one handle
+            lms_ctx.wait(h)
+            torch.cuda.synchronize()
+            lms_ctx.synchronize()
+            for o in outs:
+                assert torch.equal(o.view(torch.int32), x.view(torch.int32)), n
+            lms_ctx.release(h)
+    finally:
+        lms_ctx.set_tuning(sms, 1)
