@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--fuse-swapins", action="store_true", default=True)
     ap.add_argument("--no-fuse-swapins", dest="fuse_swapins", action="store_false")
     ap.add_argument("--b0", type=int, default=0, help="skip bisection and use this no-swap batch")
+    ap.add_argument("--search", type=int, default=0,
+                    help="probes of the n_tensors bisection (0: swap every candidate tensor)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--tf32", action="store_true")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
@@ -323,7 +325,7 @@ def main():
         lms.replan(cfg)
         xb, yb = batch(nb, seed=7)
         try:
-            for _ in range(max(1, args.warmup)):
+            for _ in range(2):
                 lms.step(xb, yb)
             torch.cuda.synchronize(dev)
             ok = True
@@ -349,8 +351,25 @@ def main():
     torch.cuda.synchronize(dev)
     ctx.synchronize()
     log(f"[bench] before swapped runs: live {ctx.stats()['device_in_use'] / GIB:.2f} GiB")
-    n_try = n_t if n_t < len(order) else -1
-    fitted = try_swap(bs, n_try) or (n_try != -1 and try_swap(bs, -1))
+    # fewest tensors that fit (the rewrite's BFS order swaps the longest-lived
+    # first, so every extra tensor only adds link traffic): all of them first,
+    # then bisect on n_tensors starting from the estimate
+    N = len(order)
+    ok_ns = []
+    fitted = try_swap(bs, -1)
+    if fitted:
+        ok_ns.append(N)
+        lo_n, hi_n = 0, N
+        probe = min(max(n_t, 1), N - 1)
+        for _ in range(args.search):
+            if hi_n - lo_n <= 1 or probe <= lo_n or probe >= hi_n:
+                break
+            if try_swap(bs, probe):
+                hi_n = probe
+                ok_ns.append(probe)
+            else:
+                lo_n = probe
+            probe = (lo_n + hi_n) // 2
     if not fitted:
         # the paper's "max batch with TFLMS": bisect between B0 and the target
         lo_b, hi_b = b0, bs
@@ -363,17 +382,41 @@ def main():
         bs = lo_b
         if not try_swap(bs, -1):
             raise SystemExit("no swapped batch above B0 fits the budget")
-    plan = lms.plan
-    log(f"[bench] plan: {plan.summary()}")
+        ok_ns = [N]
     xs, ys = batch(bs, seed=7)
 
-    ctx.trace_clear()
-    ctx.reset_peaks()
-    st0 = ctx.stats()
-    clocks = Clocks(local)
-    clocks.start()
-    swap_ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps)
-    clk = clocks.stop()
+    # timed run with the fewest tensors that fitted; a run that hits the budget
+    # anyway (timing-dependent fragmentation) falls back to the next larger set
+    swap_ms = None
+    for n_use in sorted(set(ok_ns)):
+        lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
+                                 ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
+                                 swapin_fuse_distance=1))
+        try:
+            for _ in range(args.warmup):
+                lms.step(xs, ys)
+            torch.cuda.synchronize(dev)
+            ctx.trace_clear()
+            ctx.reset_peaks()
+            st0 = ctx.stats()
+            clocks = Clocks(local)
+            clocks.start()
+            swap_ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps)
+            clk = clocks.stop()
+            break
+        except RuntimeError as e:
+            if not is_oom(e):
+                raise
+            log(f"[bench] timed run OOM with n_tensors={n_use}; trying more tensors")
+            traceback.clear_frames(e.__traceback__)
+            opt.zero_grad(set_to_none=True)
+            gc.collect()
+            torch.cuda.synchronize(dev)
+            ctx.synchronize()
+    if swap_ms is None:
+        raise SystemExit("swapped run did not fit the budget")
+    plan = lms.plan
+    log(f"[bench] plan: {plan.summary()}")
     st1 = ctx.stats()
     trace = ctx.trace()
     value = bs * ws * args.steps / (swap_ms * 1e-3)
@@ -415,6 +458,36 @@ def main():
                          f"{detail['steps']} steps (swaps = identities, interp.py:168-170)"}
 
     kernels = st1["kernel_launches"] - st0["kernel_launches"]
+    # per transfer path: wire bytes over the summed spans of its transfers
+    # (CUDA events on the copy channel each transfer ran on)
+    paths = {}
+    names = {0: "copy-engine", 1: "sm-zero-copy", 2: "zvc-zero-copy"}
+    for r in trace:
+        key = f"{'d2h' if r['direction'] == 0 else 'h2d'}:{names.get(r['codec'], r['codec'])}"
+        p = paths.setdefault(key, {"bytes": 0, "logical": 0, "ms": 0.0, "n": 0})
+        p["bytes"] += r["wire_bytes"]
+        p["logical"] += r["logical_bytes"]
+        p["ms"] += r["end_ms"] - r["start_ms"]
+        p["n"] += 1
+    for p in paths.values():
+        p["wire_gbs"] = round(p["bytes"] / max(p["ms"], 1e-9) / 1e6, 2)
+        p["logical_gbs"] = round(p["logical"] / max(p["ms"], 1e-9) / 1e6, 2)
+        p["ms"] = round(p["ms"], 1)
+    dom_key = max(paths, key=lambda k: paths[k]["ms"]) if paths else None
+    link_peak = max(link.get("d2h", 0), link.get("h2d", 0)) if link else None
+    if dom_key:
+        dom_peak = link.get(dom_key.split(":")[0]) if link else None
+        achieved = paths[dom_key]["wire_gbs"]
+        roof = {"bound": "host-link", "kernel": dom_key + (" (zvc_encode_kernel/zvc_decode_kernel)"
+                                                          if "zvc" in dom_key else ""),
+                "achieved": achieved, "peak": round(dom_peak, 2) if dom_peak else None, "unit": "GB/s",
+                "frac": round(achieved / dom_peak, 4) if dom_peak else None, "traffic": None,
+                "peak_source": "pinned copy-engine copy of 512 MiB measured in this run (host link has no "
+                               "MEASURED_PEAKS entry)",
+                "algorithmic_bytes": "wire bytes of each transfer (compressed size for ZVC)"}
+    else:
+        roof = {"bound": "host-link", "achieved": None, "peak": link_peak, "unit": "GB/s", "frac": None,
+                "traffic": None}
     out = {
         "metric": "img/s at the swapped batch (4.7x the no-swap max, or the largest that fits) under an "
                   "enforced per-GPU budget (ResNet-50 224^2 fp32, TFLMS swapping)",
@@ -454,17 +527,8 @@ def main():
                  "rewrite_s": round(plan.rewrite_seconds, 3), "bisect_s": round(bisect_s, 1),
                  "graph_nodes": len(lms.graph.nodes)},
         "host_link": {k: round(v, 2) for k, v in link.items()},
-        "roofline": {
-            "bound": "host-link",
-            "kernel": "swap transfers (copy engine D2H/H2D)",
-            "achieved": round(max(d2h_rate, h2d_rate), 2),
-            "peak": round(max(link.get("d2h", 0), link.get("h2d", 0)), 2) if link else None,
-            "unit": "GB/s",
-            "frac": round(max(d2h_rate, h2d_rate) / max(link.get("d2h", 1), link.get("h2d", 1)), 4)
-            if link else None,
-            "traffic": None,
-            "peak_source": "measured in this run (pinned copy-engine, 512 MiB)",
-        },
+        "transfer_paths": paths,
+        "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_val, 2), "unit": "img/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": 4},

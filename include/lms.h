@@ -85,6 +85,10 @@ typedef struct {
   double d2h_busy_ms, h2d_busy_ms;              /* sum of transfer spans (timing=1) */
   double swap_wait_ms;  /* consumer stalls on swap-ins (timing=1): transfer_wait_total */
   double pool_driver_ms;   /* host time in cuMemMap / cuMemSetAccess / cuMemUnmap */
+  double alloc_wait_ms;    /* host time allocations spent waiting for swap-out copies */
+  double host_grow_ms;     /* host time pinning new host-pool chunks (cudaHostAlloc) */
+  uint64_t n_host_grow;    /* pinned chunks added */
+  uint64_t n_scratch_grow; /* ZVC scratch reallocations */
 } lms_stats_t;
 
 /* one measured transfer, in the TraceEvent vocabulary (sim.py:74-81) */
@@ -126,6 +130,35 @@ int lms_dev_hold_until(lms_ctx* ctx, const void* ptr, void* stream);
 /* storage layout the swap-in restores by default: strides (elements) and the
  * number of storage elements to allocate */
 int lms_handle_layout(lms_handle* h, int64_t* strides_out, int64_t* storage_elems);
+
+/* ---- static step plan ------------------------------------------------------ */
+/* A training step allocates the same sizes in the same order every
+ * iteration.  RECORD logs one step's allocations (size, alloc/free events);
+ * lms_plan_end then places them once inside one contiguous region (greedy,
+ * step_plan.h).  REPLAY serves each later step's allocations from the
+ * recorded offsets: no fragmentation, no page moves; a step that allocates
+ * differently falls back to the dynamic pool from the first mismatch on.
+ * Residency intervals are the reference's model, sim.py:116-124, :193-211. */
+enum { LMS_PLAN_OFF = 0, LMS_PLAN_RECORD = 1, LMS_PLAN_REPLAY = 2 };
+int lms_plan_begin(lms_ctx* ctx, int mode);
+/* ends the step; after RECORD it solves the placement and reserves the
+ * region (LMS_E_OOM if the region does not fit the budget: no plan) */
+int lms_plan_end(lms_ctx* ctx);
+/* drops the plan and returns its region to the pool (no planned block may be live) */
+int lms_plan_reset(lms_ctx* ctx);
+typedef struct {
+  int ready;
+  uint64_t region_bytes, lower_bound_bytes;   /* placement vs max live bytes */
+  uint64_t n_items, n_planned;
+  uint64_t hits, dynamic, diverged_steps;
+} lms_plan_info_t;
+int lms_plan_info(lms_ctx* ctx, lms_plan_info_t* out);
+/* the recorded step (after lms_plan_end of a RECORD step): up to `cap` items */
+int lms_plan_items(lms_ctx* ctx, uint64_t* sizes, int64_t* t_alloc, int64_t* t_free, size_t cap, size_t* n);
+/* the placement on its own (host only): n items with sizes and alloc/free
+ * events (free < 0: not planned) -> offsets; returns region size via *region */
+int lms_plan_solve(const uint64_t* sizes, const int64_t* t_alloc, const int64_t* t_free, size_t n,
+                   uint64_t* offsets, uint64_t* region);
 
 /* ---- host pool ------------------------------------------------------------ */
 int lms_host_alloc(lms_ctx* ctx, size_t size, void** out);

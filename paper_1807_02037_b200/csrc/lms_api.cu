@@ -15,11 +15,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <map>
 #include <mutex>
 #include <new>
 #include <stdexcept>
@@ -31,6 +33,7 @@
 #include "arena.h"
 #include "kernels.cuh"
 #include "vmm_pool.h"
+#include "step_plan.h"
 
 namespace lms {
 
@@ -154,6 +157,32 @@ struct lms_ctx {
   std::vector<DevBlk> deferred;                             // freed, waiting for their holds
   size_t deferred_bytes = 0;
 
+  // static step plan (step_plan.h): record one step's allocations, place them
+  // once inside a single region, replay the placement on later steps
+  struct PlanFreed {
+    size_t off, size;
+    void* stream;
+    uint64_t seq;
+    char* base;   // key of the block's swap-out holds
+  };
+  struct StepPlan {
+    int mode = LMS_PLAN_OFF;
+    bool ready = false;
+    std::vector<PlanItem> items;
+    std::unordered_map<char*, size_t> rec_live;   // record: ptr -> item
+    std::unordered_map<char*, size_t> rec_held;   // record: freed, waiting for its swap-out copy
+    int64_t clock = 0;
+    Block* region = nullptr;
+    char* base = nullptr;
+    size_t size = 0, lower_bound = 0;
+    size_t cursor = 0;
+    bool diverged = false;
+    std::map<size_t, std::pair<size_t, size_t>> live;  // off -> (size, item)
+    std::vector<PlanFreed> freed;
+    size_t live_bytes = 0;
+    uint64_t hits = 0, dynamic = 0, diverged_steps = 0;
+  } plan;
+
   // pinned host pool: chunks, each an arena
   struct Chunk {
     char* base;
@@ -215,6 +244,16 @@ bool holds_clear(lms_ctx* c, char* base) {
 
 // give a freed block back to the pool
 void release_block(lms_ctx* c, const DevBlk& d) {
+  if (c->plan.mode == LMS_PLAN_RECORD) {
+    // a recorded block's lifetime ends when its memory is really reusable:
+    // after its swap-out copy, not at the logical free
+    auto& P = c->plan;
+    auto it = P.rec_held.find(d.base);
+    if (it != P.rec_held.end()) {
+      P.items[it->second].t1 = P.clock++;
+      P.rec_held.erase(it);
+    }
+  }
   c->alloc_bytes -= d.size;
   c->vmm->free(d.blk, d.stream, d.seq);
 }
@@ -238,6 +277,25 @@ void reap_deferred(lms_ctx* c, bool block) {
   c->deferred.resize(w);
 }
 
+// wait for deferred frees oldest first, one block at a time, until `enough`
+// holds.  Waiting for every pending swap-out at once would drain the D2H
+// channel and leave the link idle while the compute stream produces the next
+// tensor; waiting for just the oldest keeps the later copies queued.
+template <class F>
+void reap_until(lms_ctx* c, F enough) {
+  reap_deferred(c, false);
+  if (c->deferred.empty() || enough()) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (!c->deferred.empty() && !enough()) {
+    auto it = c->holds.find(c->deferred.front().base);
+    if (it != c->holds.end())
+      for (auto* ev : it->second) cudaEventSynchronize(ev->e);
+    c->n_device_syncs++;
+    reap_deferred(c, false);
+  }
+  c->st.alloc_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 void stream_wait_on(lms_ctx* c, void* waiter, void* owner) {
   cudaEvent_t e = c->events.get();
   cudaEventRecord(e, static_cast<cudaStream_t>(owner));
@@ -256,7 +314,9 @@ int ensure_pool(lms_ctx* c) {
   }
   auto* v = new VmmPool();
   std::string err;
-  if (!v->init(c->device, limit, kFresh, &err)) {
+  size_t page = size_t(64) << 20;
+  if (const char* pm = getenv("LMS_PAGE_MB")) page = size_t(std::max(2, atoi(pm))) << 20;
+  if (!v->init(c->device, limit, kFresh, &err, page)) {
     delete v;
     return fail(LMS_E_CUDA, "device pool: " + err);
   }
@@ -285,6 +345,106 @@ int oom(lms_ctx* c, size_t size, const std::string& why) {
   return fail(LMS_E_OOM, buf);
 }
 
+// ---- static step plan -------------------------------------------------------
+
+bool in_plan(lms_ctx* c, const void* p) {
+  const char* q = static_cast<const char*>(p);
+  return c->plan.base && q >= c->plan.base && q < c->plan.base + c->plan.size;
+}
+
+size_t dev_in_use(lms_ctx* c) {
+  return c->alloc_bytes - (c->plan.region ? c->plan.size : 0) + c->plan.live_bytes;
+}
+
+void note_peak(lms_ctx* c) { c->alloc_peak = std::max(c->alloc_peak, dev_in_use(c)); }
+
+// wait until no hold on `base` is pending (its swap-out copies finished)
+void drain_holds(lms_ctx* c, char* base) {
+  while (!holds_clear(c, base)) {
+    auto it = c->holds.find(base);
+    if (it == c->holds.end()) break;
+    for (auto* ev : it->second) cudaEventSynchronize(ev->e);
+    c->n_device_syncs++;
+  }
+}
+
+// replay: serve the next recorded allocation from its planned offset.
+// Returns 1 when this request is not planned (the dynamic pool serves it).
+int plan_alloc(lms_ctx* c, size_t rsize, void* stream, void** out) {
+  auto& P = c->plan;
+  if (P.cursor >= P.items.size()) {
+    P.diverged = true;
+    return 1;
+  }
+  const size_t idx = P.cursor++;
+  const PlanItem& it = P.items[idx];
+  if (it.size != rsize) {
+    P.diverged = true;  // the step allocates differently from the recorded one
+    P.diverged_steps++;
+    return 1;
+  }
+  if (!it.planned) return 1;
+  const size_t lo = it.off, hi = it.off + it.size;
+  // a planned block still live over this range means the sequences drifted
+  auto nx = P.live.lower_bound(lo);
+  if (nx != P.live.end() && nx->first < hi) {
+    P.diverged = true;
+    P.diverged_steps++;
+    return 1;
+  }
+  if (nx != P.live.begin()) {
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second.first > lo) {
+      P.diverged = true;
+      P.diverged_steps++;
+      return 1;
+    }
+  }
+  // earlier users of the range: swap-out copies still reading it, and work
+  // on another stream, must finish first (the dynamic pool's rules)
+  const auto t0 = std::chrono::steady_clock::now();
+  bool waited = false;
+  size_t w = 0;
+  for (size_t i = 0; i < P.freed.size(); ++i) {
+    lms_ctx::PlanFreed f = P.freed[i];
+    const bool overlap = f.off < hi && lo < f.off + f.size;
+    if (overlap) {
+      if (!holds_clear(c, f.base)) {
+        drain_holds(c, f.base);
+        waited = true;
+      }
+      if (f.stream != stream && !c->vmm->clocks_.passed(f.stream, f.seq)) {
+        c->vmm->clocks_.device_wait(stream, f.stream, f.seq);
+        c->st.n_cross_stream_waits++;
+      }
+    }
+    // keep entries whose range may still be busy for some later request
+    if (!(holds_clear(c, f.base) && c->vmm->clocks_.passed(f.stream, f.seq))) P.freed[w++] = f;
+  }
+  P.freed.resize(w);
+  if (waited)
+    c->st.alloc_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  P.live[lo] = {it.size, idx};
+  P.live_bytes += it.size;
+  P.hits++;
+  c->st.n_alloc++;
+  note_peak(c);
+  *out = P.base + lo;
+  return LMS_OK;
+}
+
+void plan_free(lms_ctx* c, void* ptr, void* stream) {
+  auto& P = c->plan;
+  const size_t off = static_cast<char*>(ptr) - P.base;
+  auto it = P.live.find(off);
+  if (it == P.live.end()) return;
+  const size_t size = it->second.first;
+  P.live.erase(it);
+  P.live_bytes -= size;
+  P.freed.push_back({off, size, stream, c->vmm->clocks_.stamp(stream), static_cast<char*>(ptr)});
+  c->st.n_free++;
+}
+
 // returns LMS_OK and *out, or LMS_E_OOM.  The budget is on live pages; when
 // it is short only because freed blocks still wait for their swap-out copies
 // the call blocks until those copies land (this is what throttles a forward
@@ -295,18 +455,24 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
   VmmPool& v = *c->vmm;
   reap_deferred(c, false);
   const size_t rsize = Arena::round(size);
+  if (c->plan.mode == LMS_PLAN_REPLAY && c->plan.ready && !c->plan.diverged) {
+    rc = plan_alloc(c, rsize, stream, out);
+    if (rc == LMS_OK) return LMS_OK;
+  }
+  if (c->plan.mode == LMS_PLAN_REPLAY) c->plan.dynamic++;
   // the budget is on live bytes; the non-deferred live set only shrinks by
   // frees the caller has not made yet, so fail at once if it plus the request
   // is over (cuDNN's plan loop probes oversized workspaces and expects a
   // quick OOM); if deferred frees are in the way, wait for their copies
   if (c->alloc_bytes - c->deferred_bytes + rsize > c->limit)
     return oom(c, size, "live set plus request exceeds the budget");
-  if (c->alloc_bytes + rsize > c->limit) reap_deferred(c, true);
+  if (c->alloc_bytes + rsize > c->limit) reap_until(c, [&] { return c->alloc_bytes + rsize <= c->limit; });
   if (c->alloc_bytes + rsize > c->limit) return oom(c, size, "live set plus request exceeds the budget");
   std::string err;
   Block* b = v.alloc(size, stream, false, &err);
-  if (!b && !c->deferred.empty()) {
-    reap_deferred(c, true);
+  while (!b && !c->deferred.empty()) {  // fragmented: free the oldest deferred block and retry
+    const size_t before = c->deferred.size();
+    reap_until(c, [&] { return c->deferred.size() < before; });
     err.clear();
     b = v.alloc(size, stream, false, &err);
   }
@@ -323,13 +489,33 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
   b->tag = stream;
   c->st.n_alloc++;
   c->alloc_bytes += b->size;
-  c->alloc_peak = std::max(c->alloc_peak, c->alloc_bytes);
+  note_peak(c);
   c->mapped_peak = std::max(c->mapped_peak, v.mapped_bytes());
   *out = v.ptr(b);
+  if (c->plan.mode == LMS_PLAN_RECORD) {
+    auto& P = c->plan;
+    PlanItem it;
+    it.size = rsize;
+    it.t0 = P.clock++;
+    P.rec_live[static_cast<char*>(*out)] = P.items.size();
+    P.items.push_back(it);
+  }
   return LMS_OK;
 }
 
 bool find_dev(lms_ctx* c, const void* ptr, bool exact, DevBlk* d) {
+  if (in_plan(c, ptr)) {
+    auto& P = c->plan;
+    const size_t off = static_cast<const char*>(ptr) - P.base;
+    auto it = P.live.upper_bound(off);
+    if (it == P.live.begin()) return false;
+    --it;
+    if (off >= it->first + it->second.first || (exact && off != it->first)) return false;
+    d->base = P.base + it->first;
+    d->size = it->second.first;
+    d->blk = nullptr;
+    return true;
+  }
   Block* b = exact ? c->vmm->find(ptr) : c->vmm->containing(ptr);
   if (!b) return false;
   d->base = c->vmm->ptr(b);
@@ -341,6 +527,18 @@ bool find_dev(lms_ctx* c, const void* ptr, bool exact, DevBlk* d) {
 int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
   if (!ptr) return LMS_OK;
   if (!c->vmm || !c->vmm->owns(ptr)) return fail(LMS_E_INVALID, "lms_dev_free: pointer not from the device pool");
+  if (in_plan(c, ptr)) {
+    plan_free(c, ptr, stream);
+    return LMS_OK;
+  }
+  if (c->plan.mode == LMS_PLAN_RECORD) {
+    auto& P = c->plan;
+    auto it = P.rec_live.find(static_cast<char*>(ptr));
+    if (it != P.rec_live.end()) {
+      P.rec_held[static_cast<char*>(ptr)] = it->second;  // t1 set in release_block
+      P.rec_live.erase(it);
+    }
+  }
   DevBlk d;
   if (!find_dev(c, ptr, true, &d)) return fail(LMS_E_INVALID, "lms_dev_free: not a live allocation");
   d.stream = stream;
@@ -372,7 +570,10 @@ int host_alloc_locked(lms_ctx* c, size_t size, void** out) {
   }
   size_t grow = std::max(need, c->cfg.host_chunk ? c->cfg.host_chunk : (size_t(1) << 30));
   void* p = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaHostAlloc(&p, grow, cudaHostAllocPortable | cudaHostAllocMapped);
+  c->st.host_grow_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->st.n_host_grow++;
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(LMS_E_HOST_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
@@ -591,6 +792,7 @@ int ensure_zvc_scratch(lms_ctx* c, size_t words) {
     c->zvc_scratch = nullptr;
   }
   size_t w = std::max(words, size_t(1) << 16);
+  c->st.n_scratch_grow++;
   CK(cudaMalloc(&c->zvc_scratch, w * 4));
   c->zvc_scratch_words = w;
   return LMS_OK;
@@ -807,6 +1009,128 @@ int lms_dev_hold_until(lms_ctx* c, const void* ptr, void* stream) {
   ev->refs = 1;
   CK(cudaEventRecord(ev->e, static_cast<cudaStream_t>(stream)));
   c->holds[d.base].push_back(ev);
+  return LMS_OK;
+}
+
+int lms_plan_begin(lms_ctx* c, int mode) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  if (mode != LMS_PLAN_RECORD && mode != LMS_PLAN_REPLAY && mode != LMS_PLAN_OFF)
+    return fail(LMS_E_INVALID, "bad plan mode");
+  std::lock_guard<std::mutex> g(c->mu);
+  int rc = ensure_pool(c);
+  if (rc) return rc;
+  auto& P = c->plan;
+  if (mode == LMS_PLAN_RECORD) {
+    if (P.region) return fail(LMS_E_STATE, "a plan is active; lms_plan_reset first");
+    P.items.clear();
+    P.rec_live.clear();
+    P.rec_held.clear();
+    P.clock = 0;
+    P.ready = false;
+  } else if (mode == LMS_PLAN_REPLAY) {
+    if (!P.ready) return fail(LMS_E_STATE, "no recorded plan");
+    P.cursor = 0;
+    P.diverged = false;
+  }
+  P.mode = mode;
+  return LMS_OK;
+}
+
+int lms_plan_end(lms_ctx* c) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  auto& P = c->plan;
+  const int mode = P.mode;
+  P.mode = LMS_PLAN_OFF;
+  if (mode != LMS_PLAN_RECORD) return LMS_OK;
+  P.rec_live.clear();  // still live at the end: t1 < 0, served dynamically
+  P.rec_held.clear();
+  const uint64_t region = plan_place(P.items);
+  P.lower_bound = plan_live_peak(P.items);
+  if (region == 0) return LMS_OK;
+  // the region is one live block of the dynamic pool; it counts against the budget
+  reap_until(c, [&] { return c->alloc_bytes + region <= c->limit; });
+  if (c->alloc_bytes + region > c->limit)
+    return oom(c, region, "step plan region does not fit next to the live set");
+  std::string err;
+  Block* b = c->vmm->alloc(region, c->home ? c->home : nullptr, true, &err);
+  if (!b) return oom(c, region, "step plan region: " + err);
+  // the region's earlier users (any stream) must be done before planned reuse
+  CK(cudaDeviceSynchronize());
+  b->tag = kFresh;
+  c->alloc_bytes += b->size;
+  P.region = b;
+  P.base = c->vmm->ptr(b);
+  P.size = b->size;
+  P.live.clear();
+  P.freed.clear();
+  P.live_bytes = 0;
+  P.ready = true;
+  return LMS_OK;
+}
+
+int lms_plan_reset(lms_ctx* c) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  auto& P = c->plan;
+  if (!P.live.empty()) return fail(LMS_E_STATE, "planned blocks are still live");
+  if (P.region) {
+    for (auto& f : P.freed) drain_holds(c, f.base);
+    CK(cudaDeviceSynchronize());
+    c->alloc_bytes -= P.region->size;
+    c->vmm->free(P.region, nullptr, 0);
+    P.region = nullptr;
+  }
+  P.base = nullptr;
+  P.size = 0;
+  P.freed.clear();
+  P.items.clear();
+  P.ready = false;
+  P.mode = LMS_PLAN_OFF;
+  return LMS_OK;
+}
+
+int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
+  if (!c || !out) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  auto& P = c->plan;
+  lms_plan_info_t r{};
+  r.ready = P.ready;
+  r.region_bytes = P.size;
+  r.lower_bound_bytes = P.lower_bound;
+  r.n_items = P.items.size();
+  for (auto& it : P.items) r.n_planned += it.planned;
+  r.hits = P.hits;
+  r.dynamic = P.dynamic;
+  r.diverged_steps = P.diverged_steps;
+  *out = r;
+  return LMS_OK;
+}
+
+int lms_plan_items(lms_ctx* c, uint64_t* sizes, int64_t* t_alloc, int64_t* t_free, size_t cap, size_t* n) {
+  if (!c || !n) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  auto& it = c->plan.items;
+  for (size_t i = 0; i < it.size() && i < cap; ++i) {
+    if (sizes) sizes[i] = it[i].size;
+    if (t_alloc) t_alloc[i] = it[i].t0;
+    if (t_free) t_free[i] = it[i].t1;
+  }
+  *n = it.size();
+  return LMS_OK;
+}
+
+int lms_plan_solve(const uint64_t* sizes, const int64_t* t_alloc, const int64_t* t_free, size_t n,
+                   uint64_t* offsets, uint64_t* region) {
+  if ((n && (!sizes || !t_alloc || !t_free || !offsets)) || !region) return fail(LMS_E_INVALID, "null argument");
+  std::vector<PlanItem> it(n);
+  for (size_t i = 0; i < n; ++i) {
+    it[i].size = sizes[i];
+    it[i].t0 = t_alloc[i];
+    it[i].t1 = t_free[i];
+  }
+  *region = plan_place(it);
+  for (size_t i = 0; i < n; ++i) offsets[i] = it[i].planned ? it[i].off : UINT64_MAX;
   return LMS_OK;
 }
 
@@ -1100,7 +1424,7 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   reap_deferred(c, false);
   account_zvc(c);
   lms_stats_t s = c->st;
-  s.device_in_use = c->alloc_bytes;
+  s.device_in_use = dev_in_use(c);
   s.device_peak = c->alloc_peak;
   s.device_reserved = c->vmm ? c->vmm->va_bytes() : 0;
   s.device_limit = c->limit;

@@ -1,0 +1,109 @@
+// Static placement of one training step's device allocations.
+//
+// A swapped training step allocates the same sizes in the same order every
+// iteration.  After one recorded step the pool knows each allocation's size
+// and lifetime (alloc event .. free event on one logical clock), so it can
+// place all of them once, offline, inside one contiguous region: no
+// fragmentation, no page moves, no allocator search on the hot path.  The
+// reference's memory model is the same idea in discrete form: residency is
+// a per-tensor interval between "alloc at op start" and "free at refcount 0"
+// (sim.py:116-124, :193-211).
+//
+// Placement is greedy: items in a priority order, each at the lowest offset
+// whose range is free for its whole lifetime.  Two orders are tried (size
+// descending; size x lifetime descending) and the smaller region wins.  No
+// CUDA here, so it is unit-testable on the host (lms_plan_solve).
+#pragma once
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+namespace lms {
+
+struct PlanItem {
+  uint64_t size = 0;   // bytes (already rounded to the pool's granule)
+  int64_t t0 = 0;      // alloc event
+  int64_t t1 = -1;     // free event; < 0: outlives the step (not planned)
+  uint64_t off = 0;    // placement (valid when planned)
+  bool planned = false;
+};
+
+namespace detail {
+
+inline uint64_t place_in_order(std::vector<PlanItem>& it, const std::vector<size_t>& order,
+                               std::vector<uint64_t>* offs) {
+  offs->assign(it.size(), 0);
+  std::vector<size_t> placed;
+  placed.reserve(order.size());
+  std::vector<std::pair<uint64_t, uint64_t>> busy;
+  uint64_t top = 0;
+  for (size_t i : order) {
+    busy.clear();
+    for (size_t j : placed)
+      if (it[j].t0 < it[i].t1 && it[i].t0 < it[j].t1) busy.emplace_back((*offs)[j], (*offs)[j] + it[j].size);
+    std::sort(busy.begin(), busy.end());
+    uint64_t off = 0;
+    for (auto& b : busy) {
+      if (b.first >= off + it[i].size) break;  // the gap before b fits
+      off = std::max(off, b.second);
+    }
+    (*offs)[i] = off;
+    top = std::max(top, off + it[i].size);
+    placed.push_back(i);
+  }
+  return top;
+}
+
+}  // namespace detail
+
+// Place every item with t1 >= 0; returns the region size.  Items with t1 < 0
+// stay unplanned (the dynamic pool serves them).
+inline uint64_t plan_place(std::vector<PlanItem>& it) {
+  std::vector<size_t> idx;
+  for (size_t i = 0; i < it.size(); ++i) {
+    it[i].planned = it[i].t1 >= 0 && it[i].t1 > it[i].t0;
+    if (it[i].planned) idx.push_back(i);
+  }
+  if (idx.empty()) return 0;
+  auto by_size = idx;
+  std::stable_sort(by_size.begin(), by_size.end(), [&](size_t a, size_t b) {
+    if (it[a].size != it[b].size) return it[a].size > it[b].size;
+    return it[a].t0 < it[b].t0;
+  });
+  auto by_area = idx;
+  std::stable_sort(by_area.begin(), by_area.end(), [&](size_t a, size_t b) {
+    const double aa = double(it[a].size) * double(it[a].t1 - it[a].t0);
+    const double bb = double(it[b].size) * double(it[b].t1 - it[b].t0);
+    if (aa != bb) return aa > bb;
+    return it[a].t0 < it[b].t0;
+  });
+  std::vector<uint64_t> o1, o2;
+  const uint64_t s1 = detail::place_in_order(it, by_size, &o1);
+  const uint64_t s2 = detail::place_in_order(it, by_area, &o2);
+  const auto& best = s1 <= s2 ? o1 : o2;
+  for (size_t i : idx) it[i].off = best[i];
+  return std::min(s1, s2);
+}
+
+// max over time of the bytes live at once: the lower bound any placement
+// of these lifetimes needs
+inline uint64_t plan_live_peak(const std::vector<PlanItem>& it) {
+  std::vector<std::pair<int64_t, int64_t>> ev;
+  for (auto& x : it)
+    if (x.planned) {
+      ev.emplace_back(x.t0, int64_t(x.size));
+      ev.emplace_back(x.t1, -int64_t(x.size));
+    }
+  std::sort(ev.begin(), ev.end());  // frees (negative) sort first at equal times
+  int64_t cur = 0, peak = 0;
+  for (auto& e : ev) {
+    cur += e.second;
+    peak = std::max(peak, cur);
+  }
+  return uint64_t(peak);
+}
+
+}  // namespace lms

@@ -51,7 +51,9 @@ _STAT_FIELDS = [
 class _Stats(ctypes.Structure):
     _fields_ = [(f, ctypes.c_uint64) for f in _STAT_FIELDS] + [
         ("d2h_busy_ms", ctypes.c_double), ("h2d_busy_ms", ctypes.c_double),
-        ("swap_wait_ms", ctypes.c_double), ("pool_driver_ms", ctypes.c_double)]
+        ("swap_wait_ms", ctypes.c_double), ("pool_driver_ms", ctypes.c_double),
+        ("alloc_wait_ms", ctypes.c_double), ("host_grow_ms", ctypes.c_double),
+        ("n_host_grow", ctypes.c_uint64), ("n_scratch_grow", ctypes.c_uint64)]
 
 
 class _Xfer(ctypes.Structure):
@@ -59,6 +61,15 @@ class _Xfer(ctypes.Structure):
                 ("logical_bytes", ctypes.c_uint64), ("wire_bytes", ctypes.c_uint64),
                 ("start_ms", ctypes.c_double), ("end_ms", ctypes.c_double)]
 
+
+class _PlanInfo(ctypes.Structure):
+    _fields_ = [("ready", ctypes.c_int), ("region_bytes", ctypes.c_uint64),
+                ("lower_bound_bytes", ctypes.c_uint64), ("n_items", ctypes.c_uint64),
+                ("n_planned", ctypes.c_uint64), ("hits", ctypes.c_uint64), ("dynamic", ctypes.c_uint64),
+                ("diverged_steps", ctypes.c_uint64)]
+
+
+PLAN_OFF, PLAN_RECORD, PLAN_REPLAY = 0, 1, 2
 
 _lib = None
 
@@ -82,6 +93,11 @@ def lib():
         "lms_set_home_stream": ([vp, vp], i), "lms_set_limit": ([vp, sz], i),
         "lms_reset_peaks": ([vp], i), "lms_get_streams": ([vp, pp, pp], i),
         "lms_set_tuning": ([vp, i, i], i),
+        "lms_plan_begin": ([vp, i], i), "lms_plan_end": ([vp], i), "lms_plan_reset": ([vp], i),
+        "lms_plan_info": ([vp, ctypes.POINTER(_PlanInfo)], i),
+        "lms_plan_items": ([vp, ctypes.POINTER(ctypes.c_uint64), i64p, i64p, sz, ctypes.POINTER(sz)], i),
+        "lms_plan_solve": ([ctypes.POINTER(ctypes.c_uint64), i64p, i64p, sz, ctypes.POINTER(ctypes.c_uint64),
+                            ctypes.POINTER(ctypes.c_uint64)], i),
         "lms_dev_alloc": ([vp, sz, vp, pp], i), "lms_dev_free": ([vp, vp, vp], i),
         "lms_dev_hold_until": ([vp, vp, vp], i),
         "lms_host_alloc": ([vp, sz, pp], i), "lms_host_free": ([vp, vp], i),
@@ -194,6 +210,31 @@ class Context:
 
     def synchronize(self):
         _check(lib().lms_synchronize(self.ptr), "lms_synchronize")
+
+    # -- static step plan -------------------------------------------------------
+    def plan_begin(self, mode: int):
+        """Start a step in PLAN_RECORD or PLAN_REPLAY mode (see include/lms.h)."""
+        _check(lib().lms_plan_begin(self.ptr, mode), "lms_plan_begin")
+
+    def plan_end(self):
+        """End the step; after a recorded one, place it (LmsOutOfMemoryError: no plan)."""
+        _check(lib().lms_plan_end(self.ptr), "lms_plan_end")
+
+    def plan_items(self, cap: int = 1 << 16):
+        """The recorded step: list of (size, alloc event, free event)."""
+        u64 = (ctypes.c_uint64 * cap)()
+        a, b = (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)()
+        n = ctypes.c_size_t()
+        _check(lib().lms_plan_items(self.ptr, u64, a, b, cap, ctypes.byref(n)), "lms_plan_items")
+        return [(u64[i], a[i], b[i]) for i in range(min(cap, n.value))]
+
+    def plan_reset(self):
+        _check(lib().lms_plan_reset(self.ptr), "lms_plan_reset")
+
+    def plan_info(self) -> dict:
+        s = _PlanInfo()
+        _check(lib().lms_plan_info(self.ptr, ctypes.byref(s)), "lms_plan_info")
+        return {f: getattr(s, f) for f, _ in _PlanInfo._fields_}
 
     # -- swap engine ------------------------------------------------------------
     def swap_out(self, t, codec: str | int = "ce", stream=None) -> SwapHandle:
@@ -308,6 +349,17 @@ class Context:
 
     def trace_clear(self):
         _check(lib().lms_trace_clear(self.ptr), "lms_trace_clear")
+
+
+def plan_solve(sizes, t_alloc, t_free):
+    """Host-only placement (step_plan.h): offsets (None = not planned) and region size."""
+    n = len(sizes)
+    u64 = ctypes.c_uint64 * max(1, n)
+    offs = u64()
+    region = ctypes.c_uint64()
+    _check(lib().lms_plan_solve(u64(*sizes), _i64(list(t_alloc)), _i64(list(t_free)), n, offs,
+                                ctypes.byref(region)), "lms_plan_solve")
+    return [None if offs[i] == 2 ** 64 - 1 else offs[i] for i in range(n)], region.value
 
 
 _installed: Context | None = None

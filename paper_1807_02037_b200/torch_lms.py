@@ -535,8 +535,13 @@ class LMS:
     """
 
     def __init__(self, model, loss_fn, optimizer, cfg: RewriteConfig, ctx: rt.Context,
-                 codec="ce", min_swap_bytes: int = 1 << 16):
+                 codec="ce", min_swap_bytes: int = 1 << 16, static_plan: bool = True):
         self.model, self.loss_fn, self.optimizer = model, loss_fn, optimizer
+        # static step plan (include/lms.h): step 0 after a (re)plan runs on the
+        # dynamic pool, step 1 is recorded and placed, later steps replay it
+        self.static_plan = static_plan
+        self._plan_step = 0
+        self.plan_note = None
         self.cfg = cfg
         self.ctx = ctx
         self.codec = codec
@@ -558,14 +563,48 @@ class LMS:
 
     def replan(self, cfg: RewriteConfig):
         """Re-run the rewrite with new knobs on the captured graph (no re-trace)."""
+        self._drop_step_plan()
         self.cfg = cfg
         self.plan = build_plan(self.graph, self.meta, cfg, 0)
         self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
         return self.plan
 
+    def _drop_step_plan(self):
+        if self._plan_step >= 2 or self.plan_note == "region":
+            torch.cuda.synchronize()
+            self.ctx.plan_reset()
+        self._plan_step = 0
+        self.plan_note = None
+
     def step(self, x, y):
         """One swapped training step; returns the loss tensor (on device)."""
-        self.optimizer.zero_grad(set_to_none=True)
-        loss = self._exec.run(lambda: self.loss_fn(self.model(x), y))
-        self.optimizer.step()
+        mode = rt.PLAN_OFF
+        if self.static_plan and self.plan_note != "no-fit":
+            mode = rt.PLAN_RECORD if self._plan_step == 1 else rt.PLAN_REPLAY if self._plan_step >= 2 else rt.PLAN_OFF
+        if mode == rt.PLAN_RECORD:
+            torch.cuda.synchronize()
+            self.ctx.plan_reset()       # a plan left over from a failed step
+        if mode != rt.PLAN_OFF:
+            self.ctx.plan_begin(mode)
+        try:
+            self.optimizer.zero_grad(set_to_none=True)
+            loss = self._exec.run(lambda: self.loss_fn(self.model(x), y))
+            self.optimizer.step()
+        except BaseException:
+            if mode != rt.PLAN_OFF:
+                self.ctx.plan_end()
+            self.optimizer.zero_grad(set_to_none=True)
+            try:
+                self._drop_step_plan()
+            except rt.LmsError:
+                self._plan_step = 0
+            raise
+        if mode != rt.PLAN_OFF:
+            try:
+                self.ctx.plan_end()
+                if mode == rt.PLAN_RECORD:
+                    self.plan_note = "region"
+            except rt.LmsOutOfMemoryError:
+                self.plan_note = "no-fit"   # the placement does not fit: stay dynamic
+        self._plan_step += 1
         return loss

@@ -76,3 +76,45 @@ def test_swapped_training_matches_plain(lms_ctx, codec, cfg):
         assert err <= 1e-5, n
     st = lms_ctx.stats()
     assert st["n_swap_out"] > 0 and st["n_swap_in"] > 0
+
+
+@pytest.mark.parametrize("codec", ["ce", "auto"])
+def test_static_plan_replay_matches_plain(lms_ctx, codec):
+    """Steps 2+ run from the recorded placement (include/lms.h, static step
+    plan): every planned allocation is served from the plan and training is
+    bit-identical to the plain run."""
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    base = _net()
+    swp = copy.deepcopy(base)
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    x = torch.randn(6, 32, 3, 32, 32, device="cuda", generator=gen)
+    y = torch.randint(0, 10, (6, 32), device="cuda", generator=gen)
+    loss_fn = torch.nn.functional.cross_entropy
+    opt_a = torch.optim.SGD(base.parameters(), lr=0.1, momentum=0.9)
+
+    def plain(xb, yb):
+        opt_a.zero_grad(set_to_none=True)
+        loss = loss_fn(base(xb), yb)
+        loss.backward()
+        opt_a.step()
+        return loss
+
+    opt_b = torch.optim.SGD(swp.parameters(), lr=0.1, momentum=0.9)
+    lms = LMS(swp, loss_fn, opt_b, RewriteConfig(fuse_swapins=True), lms_ctx, codec=codec, min_swap_bytes=0)
+    lms.capture(x[0], y[0])
+    swp.load_state_dict(base.state_dict())
+    before = lms_ctx.plan_info()
+    la = _train(base, plain, 6, x, y)
+    lb = _train(swp, lms.step, 6, x, y)
+    torch.cuda.synchronize()
+    info = lms_ctx.plan_info()
+    assert info["ready"] and info["n_planned"] > 0
+    assert info["hits"] - before["hits"] >= 3 * info["n_planned"]   # steps 2..5 replayed
+    assert info["diverged_steps"] == before["diverged_steps"]
+    assert info["region_bytes"] >= info["lower_bound_bytes"]
+    assert la == lb
+    for pa, pb in zip(base.parameters(), swp.parameters()):
+        assert torch.equal(pa, pb)
+    lms.replan(lms.cfg)   # drops the plan and returns its region
+    assert not lms_ctx.plan_info()["ready"]
