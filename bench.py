@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--arch", default="resnet50")
+    ap.add_argument("--arch", default="resnet50", help="torchvision classifier name, or unet3d")
+    ap.add_argument("--size", type=int, default=0, help="input edge (224 for classifiers, 192 for unet3d)")
     ap.add_argument("--budget-gib", type=float, default=16.0)
     ap.add_argument("--factor", type=float, default=4.7)
     ap.add_argument("--codec", default="auto", choices=["ce", "sm", "zvc", "auto"])
@@ -191,7 +192,14 @@ def main():
     torch.backends.cuda.matmul.allow_tf32 = bool(args.tf32)
 
     torch.manual_seed(0)
-    model = getattr(torchvision.models, args.arch)().to(dev)
+    size = args.size or (192 if args.arch == "unet3d" else 224)
+    if args.arch == "unet3d":
+        from paper_1807_02037_b200.workloads import unet3d
+        model = unet3d().to(dev)
+        shape_desc = f"3D U-Net {size}^3 1-channel, 2 classes, fp32"
+    else:
+        model = getattr(torchvision.models, args.arch)().to(dev)
+        shape_desc = f"{args.arch} {size}^2 fp32"
     base_model = model
     if ws > 1:
         model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
@@ -200,7 +208,10 @@ def main():
 
     def batch(n, seed=0):
         g = torch.Generator(device=dev).manual_seed(seed + rank)
-        return (torch.randn(n, 3, 224, 224, device=dev, generator=g),
+        if args.arch == "unet3d":
+            return (torch.randn(n, 1, size, size, size, device=dev, generator=g),
+                    torch.randint(0, 2, (n, size, size, size), device=dev, generator=g))
+        return (torch.randn(n, 3, size, size, device=dev, generator=g),
                 torch.randint(0, 1000, (n,), device=dev, generator=g))
 
     def plain_step(x, y):
@@ -266,7 +277,7 @@ def main():
     bisect_s = time.perf_counter() - t_bis
     log(f"[bench] budget {budget / GIB:.1f} GiB: no-swap max batch B0={b0} ({bisect_s:.1f}s)")
     if b0 == 0:
-        raise SystemExit("budget too small for batch 1")
+        log("[bench] no-swap OOM at batch 1 (the paper's 3DUnet 192^3 case, PAPER.md:1003)")
 
     # peak(B) ~ fixed + per_img * B, from the bisection's successful trials
     pts = sorted(peaks.items())
@@ -278,17 +289,19 @@ def main():
         per_img, fixed = budget / max(b0, 1), 0.0
 
     # ---- 2. no-swap throughput at B0 -----------------------------------------
-    x0, y0 = batch(b0)
-    for _ in range(args.warmup):
-        plain_step(x0, y0)
-    noswap_ms = timed(torch, dev, ws, lambda: plain_step(x0, y0), args.steps)
-    noswap_ips = b0 * ws * args.steps / (noswap_ms * 1e-3)
-    x0 = y0 = None
-    gc.collect()
-    log(f"[bench] no-swap B0={b0}: {noswap_ips:.1f} img/s ({noswap_ms / args.steps:.1f} ms/step)")
+    noswap_ms = noswap_ips = None
+    if b0 > 0:
+        x0, y0 = batch(b0)
+        for _ in range(args.warmup):
+            plain_step(x0, y0)
+        noswap_ms = timed(torch, dev, ws, lambda: plain_step(x0, y0), args.steps)
+        noswap_ips = b0 * ws * args.steps / (noswap_ms * 1e-3)
+        x0 = y0 = None
+        gc.collect()
+        log(f"[bench] no-swap B0={b0}: {noswap_ips:.1f} img/s ({noswap_ms / args.steps:.1f} ms/step)")
 
     # ---- 3. capture + rewrite, choose how many tensors to swap ----------------
-    bs = int(math.ceil(args.factor * b0))
+    bs = max(1, int(math.ceil(args.factor * b0)))
     cap_b = 4
     xc, yc = batch(cap_b)
     cfg0 = RewriteConfig(lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
@@ -452,9 +465,11 @@ def main():
     cpu = None
     if rank == 0 and args.cpu_baseline:
         from oracle.cpu_step import resnet_cpu_step_rate
-        ips, cores, detail = resnet_cpu_step_rate(args.arch, batch=8, steps=2, warmup=1, budget_s=20)
-        cpu = {"value": round(ips, 3), "unit": "img/s", "cores": cores, "kind": "port",
-               "sample": f"{args.arch} fp32 train step on host cores, batch {detail['batch']}, "
+        ips, cores, detail = resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=2, warmup=1,
+                                                  budget_s=20, image=cpu_size(args))
+        cpu = {"value": round(ips, 3), "unit": unit_name(args), "cores": cores, "kind": "port",
+               "sample": f"{args.arch} fp32 train step on host cores, batch {detail['batch']} at "
+                         f"{cpu_size(args)} px/voxels per edge, "
                          f"{detail['steps']} steps (swaps = identities, interp.py:168-170)"}
 
     kernels = st1["kernel_launches"] - st0["kernel_launches"]
@@ -489,10 +504,9 @@ def main():
         roof = {"bound": "host-link", "achieved": None, "peak": link_peak, "unit": "GB/s", "frac": None,
                 "traffic": None}
     out = {
-        "metric": "img/s at the swapped batch (4.7x the no-swap max, or the largest that fits) under an "
-                  "enforced per-GPU budget (ResNet-50 224^2 fp32, TFLMS swapping)",
+        "metric": metric_name(args),
         "value": round(value, 2),
-        "unit": "img/s",
+        "unit": unit_name(args),
         "n_gpus": ws,
         "steps": steps,
         "warmup": args.warmup,
@@ -502,18 +516,20 @@ def main():
         "vs_baseline": None,
         "dtype": "tf32" if args.tf32 else "f32",
         "data": "synthetic (randn images, randint labels; random-init torchvision weights)",
-        "config": {"workload": f"{args.arch} 224^2 fp32 training, batch {bs}/GPU = {bs / b0:.2f} x B0 "
+        "config": {"workload": f"{shape_desc} training, batch {bs}/GPU = "
+                               f"{(f'{bs / b0:.2f} x B0' if b0 else 'no-swap OOM at batch 1')} "
                                f"(target {args.factor} x) under a {budget / GIB:.0f} GiB per-GPU pool budget",
                    "model": args.arch, "global_batch": bs * ws, "per_gpu_batch": bs,
                    "budget_gib": budget / GIB, "no_swap_max_batch": b0,
-                   "batch_ratio": round(bs / b0, 3),
+                   "batch_ratio": round(bs / b0, 3) if b0 else None, "input_size": size,
                    "parallelism": f"dp{ws}" if ws > 1 else "single",
                    "l2": "inputs (>=450 MB/step) exceed L2; no flush",
                    "rewrite": {"lb": args.lb, "ub": args.ub, "ctrld_strategy": args.strategy,
                                "fuse_swapins": args.fuse_swapins, "n_tensors": plan.report.tensors_swapped},
                    "codec": args.codec},
-        "no_swap": {"batch": b0, "img_s": round(noswap_ips, 2), "ms_per_step": round(noswap_ms / steps, 3)},
-        "overhead": {"paper_framing": round(noswap_ips / value - 1.0, 4),
+        "no_swap": {"batch": b0, "img_s": round(noswap_ips, 2) if noswap_ips else None,
+                    "ms_per_step": round(noswap_ms / steps, 3) if noswap_ms else None},
+        "overhead": {"paper_framing": round(noswap_ips / value - 1.0, 4) if noswap_ips else None,
                      "note": "img/s at B0 without swap / img/s at 4.7xB0 with swap - 1"},
         "swap": {"tensors_swapped": plan.report.tensors_swapped, "swap_ins": len(plan.groups),
                  "control_edges": plan.report.control_edges_added,
@@ -530,7 +546,7 @@ def main():
         "transfer_paths": paths,
         "roofline": roof,
         "cpu_baseline": cpu,
-        "e2e": {"value": round(e2e_val, 2), "unit": "img/s", "h2d_bytes_per_step": h2d_bytes,
+        "e2e": {"value": round(e2e_val, 2), "unit": unit_name(args), "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": kernels,
         "clocks": clk,
@@ -541,6 +557,17 @@ def main():
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+
+
+def unit_name(args) -> str:
+    return "samples/s" if args.arch == "unet3d" else "img/s"
+
+
+def metric_name(args) -> str:
+    what = (f"3D U-Net {args.size or 192}^3 fp32" if args.arch == "unet3d"
+            else f"{args.arch} {args.size or 224}^2 fp32")
+    return (f"{unit_name(args)} at the swapped batch ({args.factor}x the no-swap max, or the largest that fits) "
+            f"under an enforced {args.budget_gib:g} GiB per-GPU budget ({what}, TFLMS swapping)")
 
 
 def timed(torch, dev, ws, fn, steps):
@@ -567,33 +594,46 @@ def timed(torch, dev, ws, fn, steps):
     return ms
 
 
+def cpu_batch(args) -> int:
+    return 1 if args.arch == "unet3d" else 8
+
+
+def cpu_size(args) -> int:
+    # bounded CPU sample: a 3D U-Net step at 192^3 is ~40 s of host work, so the
+    # sample is one 96^3 volume (1/8 of the voxels; stated in the JSON)
+    return 96 if args.arch == "unet3d" else (args.size or 224)
+
+
 def run_reference(args, ws, rank):
     if ws > 1 and rank != 0:
         return
     from oracle.cpu_step import resnet_cpu_step_rate
     rates = []
     for _ in range(max(1, args.warmup)):
-        resnet_cpu_step_rate(args.arch, batch=8, steps=1, warmup=0, budget_s=60)
+        resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=1, warmup=0, budget_s=60,
+                             image=cpu_size(args))
     t0 = time.perf_counter()
     cores = None
     for _ in range(args.steps):
-        ips, cores, _ = resnet_cpu_step_rate(args.arch, batch=8, steps=1, warmup=0, budget_s=60)
+        ips, cores, _ = resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=1, warmup=0, budget_s=60,
+                                             image=cpu_size(args))
         rates.append(ips)
     dt = time.perf_counter() - t0
-    value = 8 * args.steps / dt
+    value = cpu_batch(args) * args.steps / dt
     out = {
         "impl": "reference",
-        "metric": "img/s at 4.7x the no-swap max batch under an enforced per-GPU budget "
-                  "(ResNet-50 224^2 fp32, TFLMS swapping)",
-        "value": round(value, 3), "unit": "img/s", "n_gpus": ws, "steps": args.steps,
+        "metric": metric_name(args),
+        "value": round(value, 3), "unit": unit_name(args), "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": f"{args.arch} 224^2 fp32 training step on host cores "
-                                                    f"(bounded sample: batch 8 per step)",
+        "data": "synthetic", "config": {"workload": f"{args.arch} fp32 training step on host cores "
+                                                    f"(bounded sample: batch {cpu_batch(args)} at edge "
+                                                    f"{cpu_size(args)} per step)",
                                         "model": args.arch},
-        "cpu_baseline": {"value": round(value, 3), "unit": "img/s", "cores": cores, "kind": "port",
-                         "sample": "batch 8 per step; reference executor semantics: swaps are identities"},
-        "e2e": {"value": round(value, 3), "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(value, 3), "unit": unit_name(args), "cores": cores, "kind": "port",
+                         "sample": f"batch {cpu_batch(args)} at edge {cpu_size(args)} per step; reference "
+                                   "executor semantics: swaps are identities (interp.py:168-170)"},
+        "e2e": {"value": round(value, 3), "unit": unit_name(args), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 

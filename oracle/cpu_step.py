@@ -25,11 +25,17 @@ def resnet_cpu_step_rate(arch: str = "resnet50", batch: int = 8, steps: int = 3,
     threads = threads or len(os.sched_getaffinity(0))
     torch.set_num_threads(threads)
     torch.manual_seed(0)
-    model = getattr(torchvision.models, arch)()
+    if arch == "unet3d":
+        from paper_1807_02037_b200.workloads import unet3d   # the model definition only
+        model = unet3d()
+        x = torch.randn(batch, 1, image, image, image)
+        y = torch.randint(0, 2, (batch, image, image, image))
+    else:
+        model = getattr(torchvision.models, arch)()
+        x = torch.randn(batch, 3, image, image)
+        y = torch.randint(0, 1000, (batch,))
     model.train()
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
-    x = torch.randn(batch, 3, image, image)
-    y = torch.randint(0, 1000, (batch,))
 
     def step():
         opt.zero_grad(set_to_none=True)

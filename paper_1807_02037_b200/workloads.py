@@ -75,3 +75,58 @@ def ffchain_inputs(g: CompGraph, n: int, seed: int = 0) -> dict[str, np.ndarray]
             scale = 1.0 if nd.name == "x" else 1.0 / np.sqrt(n)
             out[nd.name] = rng.standard_normal((n, n)) * scale
     return out
+
+
+# ---------------------------------------------------------------------------
+# 3D U-Net (BASELINE config 3): the Çiçek et al. layout the paper trains at
+# 192^3.  Built from torch.nn modules; it is a workload
+# for the swap path, not part of the path itself.
+
+def unet3d(in_channels: int = 1, classes: int = 2, base: int = 32, depth: int = 3):
+    """3D U-Net: per level two (3x3x3 conv, BN, ReLU); 2x max-pool down,
+    2x transposed-conv up, skip concatenation; 1x1x1 conv head.  Channels
+    base, 2base, ... doubling per level (Çiçek: 32/64 .. 256/512)."""
+    import torch
+    from torch import nn
+
+    def block(cin, cmid, cout):
+        return nn.Sequential(
+            nn.Conv3d(cin, cmid, 3, padding=1, bias=False), nn.BatchNorm3d(cmid), nn.ReLU(inplace=True),
+            nn.Conv3d(cmid, cout, 3, padding=1, bias=False), nn.BatchNorm3d(cout), nn.ReLU(inplace=True))
+
+    class UNet3D(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.down = nn.ModuleList()
+            self.pool = nn.MaxPool3d(2)
+            c = in_channels
+            outs = []
+            for lvl in range(depth):
+                cmid = base * 2 ** lvl
+                self.down.append(block(c, cmid, 2 * cmid))
+                c = 2 * cmid
+                outs.append(c)
+            self.bottom = block(c, c, 2 * c)
+            c = 2 * c
+            self.up = nn.ModuleList()
+            self.dec = nn.ModuleList()
+            for lvl in reversed(range(depth)):
+                self.up.append(nn.ConvTranspose3d(c, c, 2, stride=2))
+                skip = outs[lvl]
+                self.dec.append(block(c + skip, skip, skip))
+                c = skip
+            self.head = nn.Conv3d(c, classes, 1)
+
+        def forward(self, x):
+            skips = []
+            for d in self.down:
+                x = d(x)
+                skips.append(x)
+                x = self.pool(x)
+            x = self.bottom(x)
+            for up, dec in zip(self.up, self.dec):
+                x = up(x)
+                x = dec(torch.cat([x, skips.pop()], dim=1))
+            return self.head(x)
+
+    return UNet3D()
