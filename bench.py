@@ -183,6 +183,9 @@ def main():
     ctx = rt.Context(device=local, device_reserve=budget, host_chunk=4 * GIB, timing=True)
     rt.install_allocator(ctx)
     torch.cuda.set_device(local)
+    # the link's copy-engine peak, measured first while the pool is empty
+    link = measure_host_link(torch, dev)
+    gc.collect()
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
@@ -302,12 +305,23 @@ def main():
 
     # ---- 3. capture + rewrite, choose how many tensors to swap ----------------
     bs = max(1, int(math.ceil(args.factor * b0)))
+    # capture: one traced step of the same model at a small batch (the graph
+    # does not depend on batch or spatial size; tensor bytes scale with both)
     cap_b = 4
-    xc, yc = batch(cap_b)
+    cap_scale = 1.0 / cap_b
+    if args.arch == "unet3d":
+        cap_b, cap_size = 1, 64
+        g = torch.Generator(device=dev).manual_seed(rank)
+        xc = torch.randn(1, 1, cap_size, cap_size, cap_size, device=dev, generator=g)
+        yc = torch.randint(0, 2, (1, cap_size, cap_size, cap_size), device=dev, generator=g)
+        cap_scale = (size / cap_size) ** 3
+    else:
+        xc, yc = batch(cap_b)
     cfg0 = RewriteConfig(lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
                          fuse_swapins=args.fuse_swapins, swapin_fuse_distance=1)
     codec = args.codec
-    lms = LMS(model, loss_fn, opt, cfg0, ctx, codec=codec, min_swap_bytes=(256 << 10) // cap_b)
+    # tensors under 64 KiB at the capture size stay on the device
+    lms = LMS(model, loss_fn, opt, cfg0, ctx, codec=codec, min_swap_bytes=64 << 10)
     t_cap = time.perf_counter()
     plan = lms.capture(xc, yc)
     capture_s = time.perf_counter() - t_cap
@@ -319,7 +333,7 @@ def main():
     for _, _, tid in plan.report.edges_rewritten:
         if tid not in seen:
             seen.add(tid)
-            order.append(tid_bytes[tid] / cap_b)
+            order.append(tid_bytes[tid] * cap_scale)
     need = fixed + per_img * bs - 0.90 * budget  # bytes that must live off-device at the peak
     n_t, acc = 0, 0.0
     while n_t < len(order) and acc * bs < 1.15 * need:
@@ -453,7 +467,8 @@ def main():
     e2e_val = bs * ws * args.steps / (e2e_ms * 1e-3)
 
     # ---- 6. link peak, CPU baseline -----------------------------------------
-    link = measure_host_link(torch, dev) if rank == 0 else {}
+    if rank != 0:
+        link = {}
     d2h_b = st1["d2h_wire_bytes"]
     h2d_b = st1["h2d_wire_bytes"]
     steps = args.steps
@@ -541,7 +556,8 @@ def main():
                  "device_peak_bytes": st1["device_peak"], "host_peak_bytes": st1["host_peak"],
                  "attempts": attempts, "capture_s": round(capture_s, 2),
                  "rewrite_s": round(plan.rewrite_seconds, 3), "bisect_s": round(bisect_s, 1),
-                 "graph_nodes": len(lms.graph.nodes)},
+                 "graph_nodes": len(lms.graph.nodes), "static_plan": lms.plan_note,
+                 "plan_info": ctx.plan_info()},
         "host_link": {k: round(v, 2) for k, v in link.items()},
         "transfer_paths": paths,
         "roofline": roof,

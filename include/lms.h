@@ -89,6 +89,7 @@ typedef struct {
   double host_grow_ms;     /* host time pinning new host-pool chunks (cudaHostAlloc) */
   uint64_t n_host_grow;    /* pinned chunks added */
   uint64_t n_scratch_grow; /* ZVC scratch reallocations */
+  double unmap_ms, map_ms, access_ms;  /* pool_driver_ms split by driver call */
 } lms_stats_t;
 
 /* one measured transfer, in the TraceEvent vocabulary (sim.py:74-81) */
@@ -115,10 +116,12 @@ int lms_set_home_stream(lms_ctx* ctx, void* stream);
 int lms_set_limit(lms_ctx* ctx, size_t limit);
 int lms_reset_peaks(lms_ctx* ctx);
 int lms_get_streams(lms_ctx* ctx, void** d2h, void** h2d);
-/* Tuning of the zero-copy kernels: CTAs per launch (0 = keep) and whether the
- * ZVC kernels move chunks with bulk async copies (1, TMA path) or with
- * per-thread 16 B loads/stores (0); -1 keeps the current setting. */
-int lms_set_tuning(lms_ctx* ctx, int zc_ctas, int use_bulk);
+/* Tuning: CTAs per zero-copy kernel launch (0 = keep); whether the ZVC
+ * kernels move chunks with bulk async copies (1, TMA path) or with per-thread
+ * 16 B loads/stores (0); whether pack/unpack of rows layouts in HBM go
+ * through tensor maps (1, cp.async.bulk.tensor) or the SIMT kernels (0).
+ * -1 keeps the current setting. */
+int lms_set_tuning(lms_ctx* ctx, int zc_ctas, int use_bulk, int use_tma_pack);
 
 /* ---- device pool (replaces the simulator's residency model) ------------- */
 int lms_dev_alloc(lms_ctx* ctx, size_t size, void* stream, void** out);

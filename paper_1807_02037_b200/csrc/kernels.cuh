@@ -106,6 +106,8 @@ __global__ void __launch_bounds__(256) rows_kernel(char* __restrict__ dst, const
 // transpose path: the strided side has a unit-stride dim `cd` (not the last
 // one) and its last dim is strided.  A 32x32 tile over (cd, last) is read
 // coalesced along cd and written coalesced along last through shared memory.
+// Index math is per tile (64-bit tile bases, one pass over the batch dims);
+// per element only 32-bit in-tile offsets (host checks 32*stride < 2^31).
 
 template <bool PACK, int E>
 __global__ void __launch_bounds__(256) transpose_kernel(char* __restrict__ dst, const char* __restrict__ src,
@@ -116,53 +118,74 @@ __global__ void __launch_bounds__(256) transpose_kernel(char* __restrict__ dst, 
   const int64_t nA = d.sizes[cd], nB = d.sizes[last];
   const int64_t tilesA = (nA + 31) / 32, tilesB = (nB + 31) / 32;
   const int64_t ntiles = batches * tilesA * tilesB;
-  // logical (row-major) strides of the contiguous side
+  // row-major strides of the contiguous side
   int64_t cstride[kMaxDims];
   {
     int64_t acc = 1;
+#pragma unroll
     for (int k = kMaxDims - 1; k >= 0; --k) {
-      if (k < d.ndim) { cstride[k] = acc; acc *= d.sizes[k]; }
+      if (k < d.ndim) {
+        cstride[k] = acc;
+        acc *= d.sizes[k];
+      }
     }
   }
+  const uint32_t sA = uint32_t(d.strides[cd]), sB = uint32_t(d.strides[last]);  // strided side
+  const uint32_t cA = uint32_t(cstride[cd]);                                      // contiguous side (cB = 1)
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const T* sw = reinterpret_cast<const T*>(src);
+  T* dw = reinterpret_cast<T*>(dst);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int64_t b = t / (tilesA * tilesB);
-    int64_t rem = t - b * tilesA * tilesB;
-    int64_t a0 = (rem / tilesB) * 32, b0 = (rem % tilesB) * 32;
+    const int64_t b = t / (tilesA * tilesB);
+    const int64_t rem = t - b * tilesA * tilesB;
+    const int64_t ta = rem / tilesB;
+    const int64_t a0 = ta * 32, b0 = (rem - ta * tilesB) * 32;
     // batch index -> offsets over the dims other than cd and last
     int64_t soff = 0, coff = 0, bi = b;
     for (int k = last - 1; k >= 0; --k) {
       if (k == cd) continue;
-      int64_t s = d.sizes[k];
-      int64_t q = bi / s, x = bi - q * s;
+      const int64_t s = d.sizes[k];
+      const int64_t q = bi / s;
+      const int64_t x = bi - q * s;
       soff += x * d.strides[k];
       coff += x * cstride[k];
       bi = q;
     }
-    const T* sw = reinterpret_cast<const T*>(src);
-    T* dw = reinterpret_cast<T*>(dst);
-    // phase 1 reads coalesced on the source side, phase 2 writes coalesced on
-    // the destination side; the strided side is unit-stride along cd, the
-    // contiguous side along the last dim.
+    const int ra = int(nA - a0 < 32 ? nA - a0 : 32), rb = int(nB - b0 < 32 ? nB - b0 : 32);
+    const int64_t s_org = soff + a0 * d.strides[cd] + b0 * d.strides[last];  // strided-side tile origin
+    const int64_t c_org = coff + a0 * cstride[cd] + b0;                       // contiguous-side tile origin
+    T v[4];
     if (PACK) {
-      for (int j = ty; j < 32; j += 8) {
-        int64_t ia = a0 + tx, ib = b0 + j;
-        if (ia < nA && ib < nB) tile[j][tx] = sw[soff + ia * d.strides[cd] + ib * d.strides[last]];
+      const T* sp = sw + s_org;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = ty + 8 * k;  // b (last) index; tx runs along the unit-stride a
+        v[k] = (tx < ra && j < rb) ? sp[uint32_t(tx) * sA + uint32_t(j) * sB] : T(0);
       }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tile[ty + 8 * k][tx] = v[k];
       __syncthreads();
-      for (int j = ty; j < 32; j += 8) {
-        int64_t ia = a0 + j, ib = b0 + tx;
-        if (ia < nA && ib < nB) dw[coff + ia * cstride[cd] + ib] = tile[tx][j];
+      T* cp = dw + c_org;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = ty + 8 * k;  // a index; tx runs along the contiguous b
+        if (j < ra && tx < rb) cp[uint32_t(j) * cA + tx] = tile[tx][j];
       }
     } else {
-      for (int j = ty; j < 32; j += 8) {
-        int64_t ia = a0 + j, ib = b0 + tx;
-        if (ia < nA && ib < nB) tile[j][tx] = sw[coff + ia * cstride[cd] + ib];
+      const T* cp = sw + c_org;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = ty + 8 * k;  // a index; tx runs along the contiguous b
+        v[k] = (j < ra && tx < rb) ? cp[uint32_t(j) * cA + tx] : T(0);
       }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tile[ty + 8 * k][tx] = v[k];
       __syncthreads();
-      for (int j = ty; j < 32; j += 8) {
-        int64_t ia = a0 + tx, ib = b0 + j;
-        if (ia < nA && ib < nB) dw[soff + ia * d.strides[cd] + ib * d.strides[last]] = tile[tx][j];
+      T* sp = dw + s_org;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = ty + 8 * k;  // b index; tx runs along the unit-stride a
+        if (tx < ra && j < rb) sp[uint32_t(tx) * sA + uint32_t(j) * sB] = tile[tx][j];
       }
     }
     __syncthreads();
@@ -586,6 +609,96 @@ __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict_
     }
     __syncthreads();  // chunk buffer b is free for the load issued two tiles from now
   }
+}
+
+}  // namespace lms
+
+// -------------------------------------------------------------------------
+// TMA pack/unpack ("rows" layouts): both sides are described by 5-D tensor
+// maps with identical logical dims (innermost unit-stride on both); a
+// single elected thread per CTA walks boxes through a STAGES-deep ring of
+// shared-memory buffers: cp.async.bulk.tensor load (mbarrier completion) ->
+// cp.async.bulk.tensor store.  The TMA engine does all address generation,
+// so the per-byte instruction cost is ~0 (the SIMT kernels above spend it on
+// 64-bit index math).  OOB parts of edge boxes are zero-filled on load and
+// clipped on store.  Stage buffers are 1 KiB aligned (TMA needs >= 128 B).
+
+#include <cuda.h>
+
+namespace lms {
+
+struct TmaBoxGrid {
+  uint32_t nbox[5];   // boxes per dim (innermost first)
+  uint32_t box[5];    // box extent per dim
+  uint64_t total;     // product of nbox
+};
+
+__device__ __forceinline__ void tma_load_5d(void* smem, const CUtensorMap* map, const int c[5], uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const int c[5], const void* smem) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(smem))
+               : "memory");
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(32) tma_copy_kernel(const __grid_constant__ CUtensorMap src,
+                                                      const __grid_constant__ CUtensorMap dst, TmaBoxGrid g,
+                                                      uint32_t box_bytes, uint32_t stage_bytes) {
+  extern __shared__ __align__(128) unsigned char tsm[];
+  __shared__ __align__(8) uint64_t bar[STAGES];
+  if (threadIdx.x != 0) return;  // one thread drives the TMA engine
+  for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+  fence_mbar_init();
+  auto coords = [&](uint64_t b, int c[5]) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t q = uint32_t(b % g.nbox[k]);
+      b /= g.nbox[k];
+      c[k] = int(q * g.box[k]);
+    }
+  };
+  const uint64_t step = gridDim.x;
+  uint64_t next_load = blockIdx.x, next_store = blockIdx.x;
+  uint32_t phase_bits = 0;
+  int s_load = 0, s_store = 0, inflight = 0;
+  int c[5];
+  while (inflight < STAGES && next_load < g.total) {
+    coords(next_load, c);
+    mbar_expect_tx(&bar[s_load], box_bytes);
+    tma_load_5d(tsm + size_t(s_load) * stage_bytes, &src, c, &bar[s_load]);
+    next_load += step;
+    s_load = (s_load + 1) % STAGES;
+    ++inflight;
+  }
+  while (inflight > 0) {
+    mbar_wait(&bar[s_store], (phase_bits >> s_store) & 1u);
+    phase_bits ^= 1u << s_store;
+    coords(next_store, c);
+    tma_store_5d(&dst, c, tsm + size_t(s_store) * stage_bytes);
+    bulk_commit();
+    next_store += step;
+    --inflight;
+    s_store = (s_store + 1) % STAGES;
+    if (next_load < g.total) {
+      bulk_wait_read<0>();  // the stage about to be refilled has been read by its store
+      coords(next_load, c);
+      mbar_expect_tx(&bar[s_load], box_bytes);
+      tma_load_5d(tsm + size_t(s_load) * stage_bytes, &src, c, &bar[s_load]);
+      next_load += step;
+      s_load = (s_load + 1) % STAGES;
+      ++inflight;
+    }
+  }
+  bulk_wait<0>();
 }
 
 }  // namespace lms

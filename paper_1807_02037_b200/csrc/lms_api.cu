@@ -208,6 +208,7 @@ struct lms_ctx {
   uint64_t trace_gen = 0;   // bumped by lms_trace_clear
   int use_bulk = 1;         // ZVC kernels move chunks with cp.async.bulk (LMS_ZVC_BULK=0: STG/LDG)
   int zc_ctas = 0;          // CTAs of the zero-copy (host-side) kernels
+  int use_tma_pack = 1;     // pack/unpack of rows layouts through tensor maps (LMS_TMA_PACK=0: SIMT)
   // consumer reached its wait (event on the consumer stream) vs swap-in record
   std::vector<std::pair<cudaEvent_t, int64_t>> waits;
 };
@@ -678,6 +679,111 @@ void to_desc(Strided* d, int ndim, const int64_t* sizes, const int64_t* strides)
   }
 }
 
+// ---- TMA pack/unpack --------------------------------------------------------
+
+bool is_host_ptr(const void* p);
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+constexpr int kTmaStages = 4;
+constexpr uint32_t kTmaBoxTarget = 16384;
+
+// Rows layouts (the strided side's innermost dim has unit stride) through
+// tensor maps.  sizes/strides: row-major, squeezed; strides are the strided
+// side's (elements).  Returns 1 when the layout does not qualify (the caller
+// uses the SIMT kernels), 0 on launch, <0 on error.
+template <bool PACK>
+int launch_tma_rows(lms_ctx* c, char* dst, const char* src, int nd, const int64_t* sizes, const int64_t* strides,
+                    int elem, cudaStream_t s) {
+  if (!c->use_tma_pack || nd < 1 || strides[nd - 1] != 1) return 1;
+  if (reinterpret_cast<uintptr_t>(dst) % 16 || reinterpret_cast<uintptr_t>(src) % 16) return 1;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return 1;
+  // merge row-major dims the strided side keeps adjacent
+  int64_t ms[LMS_MAX_DIMS + 1], mz[LMS_MAX_DIMS + 1];
+  int n = 0;
+  for (int k = 0; k < nd; ++k) {
+    if (n > 0 && ms[n - 1] == strides[k] * sizes[k]) {
+      mz[n - 1] *= sizes[k];
+      ms[n - 1] = strides[k];
+    } else {
+      mz[n] = sizes[k];
+      ms[n] = strides[k];
+      ++n;
+    }
+  }
+  if (n > 5) return 1;
+  cuuint64_t gdim[5], sstr[4], cstr[4];
+  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) gdim[i] = i < n ? cuuint64_t(mz[n - 1 - i]) : 1;
+  uint64_t cacc = uint64_t(elem);
+  for (int i = 1; i < 5; ++i) {
+    cacc *= gdim[i - 1];
+    cstr[i - 1] = cacc;
+    sstr[i - 1] = i < n ? uint64_t(ms[n - 1 - i]) * elem : (i == 1 ? cacc : sstr[i - 2] * gdim[i - 1]);
+  }
+  for (int i = 0; i < 4; ++i) {
+    if (gdim[i] > (uint64_t(1) << 32) || cstr[i] % 16 || sstr[i] % 16 || cstr[i] >= (uint64_t(1) << 40) ||
+        sstr[i] >= (uint64_t(1) << 40))
+      return 1;
+  }
+  // box: innermost up to 256 elements (a 16 B multiple), then fill ~16 KiB
+  uint32_t b0 = uint32_t(std::min<uint64_t>(gdim[0], 256));
+  const uint32_t q = 16 / std::min(elem, 16);
+  b0 = (b0 + q - 1) / q * q;
+  if (b0 > 256) return 1;
+  box[0] = b0;
+  uint64_t bytes = uint64_t(b0) * elem;
+  for (int i = 1; i < 5; ++i) {
+    uint64_t room = std::max<uint64_t>(1, kTmaBoxTarget / bytes);
+    box[i] = uint32_t(std::min<uint64_t>({gdim[i], room, 256}));
+    bytes *= box[i];
+  }
+  CUtensorMapDataType dt = elem == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                           : elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                           : elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                       : CU_TENSOR_MAP_DATA_TYPE_UINT64;
+  CUtensorMap ms_map, mc_map;  // strided side, contiguous side
+  const char* strided = PACK ? src : dst;
+  const char* contig = PACK ? dst : src;
+  if (enc(&ms_map, dt, 5, const_cast<char*>(strided), gdim, sstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS ||
+      enc(&mc_map, dt, 5, const_cast<char*>(contig), gdim, cstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+    return 1;
+  TmaBoxGrid g{};
+  g.total = 1;
+  for (int i = 0; i < 5; ++i) {
+    g.box[i] = box[i];
+    g.nbox[i] = uint32_t((gdim[i] + box[i] - 1) / box[i]);
+    g.total *= g.nbox[i];
+  }
+  const int grid = int(std::min<uint64_t>(g.total, uint64_t(c->num_sms) * 4));
+  const uint32_t box_bytes = uint32_t(bytes);
+  const uint32_t stage_bytes = (box_bytes + 1023) / 1024 * 1024;
+  tma_copy_kernel<kTmaStages><<<grid, 32, size_t(kTmaStages) * stage_bytes, s>>>(
+      PACK ? ms_map : mc_map, PACK ? mc_map : ms_map, g, box_bytes, stage_bytes);
+  c->st.kernel_launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
 // pack (dst contiguous) or unpack (dst strided); either side may be mapped host memory
 template <bool PACK>
 int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_t* sizes_in,
@@ -718,6 +824,10 @@ int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_
     default: KERNEL<PACK, 8><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                 \
   }
   const int last = nd - 1;
+  if (strides[last] == 1 && !is_host_ptr(dst) && !is_host_ptr(src)) {
+    int rc = launch_tma_rows<PACK>(c, dst, src, nd, sizes, strides, elem, s);
+    if (rc <= 0) return rc;
+  }
   if (strides[last] == 1) {
     int64_t row = sizes[last], rows = numel / row;
     bool vec = (row * elem) % 16 == 0 && (reinterpret_cast<uintptr_t>(dst) % 16 == 0) &&
@@ -743,7 +853,10 @@ int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_
     int cd = -1;
     for (int k = 0; k < last; ++k)
       if (strides[k] == 1) cd = k;
-    if (cd >= 0 && sizes[cd] >= 8 && sizes[last] >= 8) {
+    // the transpose kernel keeps in-tile offsets in 32 bits
+    const bool small_strides = cd >= 0 && 31 * (strides[cd] + strides[last]) < (int64_t(1) << 31) &&
+                               numel / sizes[cd] * 32 < (int64_t(1) << 31);
+    if (cd >= 0 && sizes[cd] >= 8 && sizes[last] >= 8 && small_strides) {
       int64_t batches = numel / (sizes[cd] * sizes[last]);
       int64_t tiles = batches * ((sizes[cd] + 31) / 32) * ((sizes[last] + 31) / 32);
       int grid = sm_grid(c, tiles, 1);
@@ -779,9 +892,9 @@ bool is_host_ptr(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
-    return true;
+    return true;  // unknown to CUDA: treat as host (the SIMT kernels handle both)
   }
-  return a.type == cudaMemoryTypeHost;
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
 }
 
 int ensure_zvc_scratch(lms_ctx* c, size_t words) {
@@ -878,6 +991,9 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
   c->zc_ctas = cfg->sm_ctas > 0 ? cfg->sm_ctas : c->num_sms;
   if (const char* v = getenv("LMS_ZC_CTAS")) c->zc_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("LMS_ZVC_BULK")) c->use_bulk = atoi(v) != 0;
+  if (const char* v = getenv("LMS_TMA_PACK")) c->use_tma_pack = atoi(v) != 0;
+  cudaFuncSetAttribute(tma_copy_kernel<kTmaStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kTmaStages * int(kTmaBoxTarget) * 2);
   cudaFuncSetAttribute(zvc_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
   cudaFuncSetAttribute(zvc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
   int lo = 0, hi = 0;
@@ -971,11 +1087,12 @@ int lms_reset_peaks(lms_ctx* c) {
   return LMS_OK;
 }
 
-int lms_set_tuning(lms_ctx* c, int zc_ctas, int use_bulk) {
+int lms_set_tuning(lms_ctx* c, int zc_ctas, int use_bulk, int use_tma_pack) {
   if (!c) return fail(LMS_E_INVALID, "null ctx");
   std::lock_guard<std::mutex> g(c->mu);
   if (zc_ctas > 0) c->zc_ctas = zc_ctas;
   if (use_bulk >= 0) c->use_bulk = use_bulk != 0;
+  if (use_tma_pack >= 0) c->use_tma_pack = use_tma_pack != 0;
   return LMS_OK;
 }
 
@@ -1436,6 +1553,9 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   s.n_reclaims = c->vmm ? c->vmm->n_moves() : 0;
   s.n_device_syncs = c->n_device_syncs;
   s.pool_driver_ms = c->vmm ? c->vmm->driver_ms() : 0;
+  s.unmap_ms = c->vmm ? c->vmm->unmap_ms() : 0;
+  s.map_ms = c->vmm ? c->vmm->map_ms() : 0;
+  s.access_ms = c->vmm ? c->vmm->access_ms() : 0;
   s.device_deferred_bytes = c->deferred_bytes;
   s.host_in_use = c->host_used;
   s.host_peak = c->host_peak;

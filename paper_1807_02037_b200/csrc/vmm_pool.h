@@ -258,6 +258,9 @@ class VmmPool {
   uint64_t n_unmap() const { return n_unmap_; }
   uint64_t n_moves() const { return n_moves_; }
   double driver_ms() const { return driver_s_ * 1e3; }
+  double unmap_ms() const { return unmap_s_ * 1e3; }
+  double map_ms() const { return map_s_ * 1e3; }
+  double access_ms() const { return access_s_ * 1e3; }
   size_t va_bytes() const { return small_va_ + large_va_; }
   template <class F>
   void for_each_live(F&& f) {
@@ -327,7 +330,9 @@ class VmmPool {
   void unmap_page(size_t p) {
     auto t0 = now();
     drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
-    driver_s_ += secs(t0);
+    const double dt = secs(t0);
+    driver_s_ += dt;
+    unmap_s_ += dt;
     free_.push_back(handle_of_[p]);
     handle_of_[p] = -1;
     --mapped_;
@@ -341,7 +346,10 @@ class VmmPool {
       int h = free_.back();
       free_.pop_back();
       size_t p = pages[i];
-      if (drv_.map(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_, 0, handles_[h], 0) != CUDA_SUCCESS) {
+      auto tm = now();
+      const CUresult mr = drv_.map(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_, 0, handles_[h], 0);
+      map_s_ += secs(tm);
+      if (mr != CUDA_SUCCESS) {
         free_.push_back(h);
         *err = "cuMemMap failed";
         driver_s_ += secs(t0);
@@ -353,8 +361,11 @@ class VmmPool {
       bool last = i + 1 == pages.size() || pages[i + 1] != p + 1;
       if (last) {
         size_t start = pages[run];
-        if (drv_.set_access(reinterpret_cast<CUdeviceptr>(base_ + start * page_), (p - start + 1) * page_,
-                            &access_, 1) != CUDA_SUCCESS) {
+        auto ta = now();
+        const CUresult ar = drv_.set_access(reinterpret_cast<CUdeviceptr>(base_ + start * page_),
+                                            (p - start + 1) * page_, &access_, 1);
+        access_s_ += secs(ta);
+        if (ar != CUDA_SUCCESS) {
           *err = "cuMemSetAccess failed";
           driver_s_ += secs(t0);
           return false;
@@ -389,7 +400,7 @@ class VmmPool {
   std::vector<int> free_;            // physical pages not mapped anywhere
   size_t created_ = 0, limit_pages_ = 0, mapped_ = 0, bytes_live_ = 0, live_pages_ = 0;
   uint64_t n_map_ = 0, n_unmap_ = 0, n_moves_ = 0;
-  double driver_s_ = 0;
+  double driver_s_ = 0, unmap_s_ = 0, map_s_ = 0, access_s_ = 0;
 };
 
 }  // namespace lms

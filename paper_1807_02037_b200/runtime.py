@@ -53,7 +53,8 @@ class _Stats(ctypes.Structure):
         ("d2h_busy_ms", ctypes.c_double), ("h2d_busy_ms", ctypes.c_double),
         ("swap_wait_ms", ctypes.c_double), ("pool_driver_ms", ctypes.c_double),
         ("alloc_wait_ms", ctypes.c_double), ("host_grow_ms", ctypes.c_double),
-        ("n_host_grow", ctypes.c_uint64), ("n_scratch_grow", ctypes.c_uint64)]
+        ("n_host_grow", ctypes.c_uint64), ("n_scratch_grow", ctypes.c_uint64),
+        ("unmap_ms", ctypes.c_double), ("map_ms", ctypes.c_double), ("access_ms", ctypes.c_double)]
 
 
 class _Xfer(ctypes.Structure):
@@ -92,7 +93,7 @@ def lib():
         "lms_set_global": ([vp], i), "lms_get_global": ([], vp),
         "lms_set_home_stream": ([vp, vp], i), "lms_set_limit": ([vp, sz], i),
         "lms_reset_peaks": ([vp], i), "lms_get_streams": ([vp, pp, pp], i),
-        "lms_set_tuning": ([vp, i, i], i),
+        "lms_set_tuning": ([vp, i, i, i], i),
         "lms_plan_begin": ([vp, i], i), "lms_plan_end": ([vp], i), "lms_plan_reset": ([vp], i),
         "lms_plan_info": ([vp, ctypes.POINTER(_PlanInfo)], i),
         "lms_plan_items": ([vp, ctypes.POINTER(ctypes.c_uint64), i64p, i64p, sz, ctypes.POINTER(sz)], i),
@@ -192,9 +193,10 @@ class Context:
     def set_limit(self, nbytes: int):
         _check(lib().lms_set_limit(self.ptr, nbytes), "lms_set_limit")
 
-    def set_tuning(self, zc_ctas: int = 0, use_bulk: int = -1):
-        """CTAs of the zero-copy kernels (0 = keep) and bulk-copy (TMA) use for ZVC (-1 = keep)."""
-        _check(lib().lms_set_tuning(self.ptr, zc_ctas, use_bulk), "lms_set_tuning")
+    def set_tuning(self, zc_ctas: int = 0, use_bulk: int = -1, use_tma_pack: int = -1):
+        """CTAs of the zero-copy kernels (0 = keep), bulk-copy (TMA) use for ZVC and
+        tensor-map pack/unpack (-1 = keep)."""
+        _check(lib().lms_set_tuning(self.ptr, zc_ctas, use_bulk, use_tma_pack), "lms_set_tuning")
 
     def reset_peaks(self):
         _check(lib().lms_reset_peaks(self.ptr), "lms_reset_peaks")

@@ -163,8 +163,12 @@ class _Capture:
                            t.requires_grad, isinstance(t, torch.nn.Parameter)))
         # share of all-zero 32-bit words: what the ZVC codec would drop
         zf = 0.0
-        if t.numel() and t.element_size() == 4 and not isinstance(t, torch.nn.Parameter):
-            zf = float((t.detach().view(torch.int32) == 0).sum()) / t.numel()
+        if (t.numel() and t.element_size() == 4 and t.is_contiguous()
+                and not isinstance(t, torch.nn.Parameter)):
+            w = t.detach().view(-1).view(torch.int32)
+            if w.numel() > (1 << 22):      # a strided sample: no tensor-sized temporaries
+                w = w[:: w.numel() >> 22]
+            zf = 1.0 - float(torch.count_nonzero(w)) / w.numel()
         self.zero_frac.append(zf)
         t = t.detach()   # no tensor -> grad_fn -> saved -> tensor cycle (see SwapExecutor.pack)
         self.keep.append(t)

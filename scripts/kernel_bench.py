@@ -80,7 +80,25 @@ def main():
         outs = torch.empty(vs.shape, device=dev)
         b2 = vs.numel() * 4
         t = timed(lambda: ctx.pack(vs, outs))
-        res["pack_rows"] = {"gbs": 2 * b2 / t / 1e9, "frac_hbm": 2 * b2 / t / 1e9 / hbm_peak, "ms": t * 1e3}
+        res["pack_rows_tma"] = {"gbs": 2 * b2 / t / 1e9, "frac_hbm": 2 * b2 / t / 1e9 / hbm_peak, "ms": t * 1e3}
+        assert torch.equal(outs, vs.contiguous())
+        vc = x[:, 8:40]                      # channel slice: 16 B-aligned strides, long contiguous runs
+        outc = torch.empty(vc.shape, device=dev)
+        b3 = vc.numel() * 4
+        t = timed(lambda: ctx.pack(vc, outc))
+        res["pack_channel_slice_tma"] = {"gbs": 2 * b3 / t / 1e9, "frac_hbm": 2 * b3 / t / 1e9 / hbm_peak,
+                                         "ms": t * 1e3}
+        assert torch.equal(outc, vc.contiguous())
+        ctx.set_tuning(0, -1, 0)             # the SIMT rows kernel on the same views
+        t = timed(lambda: ctx.pack(vs, outs))
+        res["pack_rows_simt"] = {"gbs": 2 * b2 / t / 1e9, "frac_hbm": 2 * b2 / t / 1e9 / hbm_peak, "ms": t * 1e3}
+        t = timed(lambda: ctx.pack(vc, outc))
+        res["pack_channel_slice_simt"] = {"gbs": 2 * b3 / t / 1e9, "frac_hbm": 2 * b3 / t / 1e9 / hbm_peak,
+                                          "ms": t * 1e3}
+        ctx.set_tuning(0, -1, 1)
+        refc = torch.empty_like(outc)
+        t = timed(lambda: refc.copy_(vc))
+        res["torch_contiguous_channel_slice"] = {"gbs": 2 * b3 / t / 1e9, "ms": t * 1e3}
         ref = torch.empty_like(out)
         t = timed(lambda: ref.copy_(v))
         res["torch_contiguous_same_view"] = {"gbs": 2 * tb / t / 1e9, "ms": t * 1e3}
@@ -90,6 +108,12 @@ def main():
         t = timed(lambda: ctx.unpack(src, v))
         assert torch.equal(v, src)
         res["unpack_transpose"] = {"gbs": 2 * tb / t / 1e9, "frac_hbm": 2 * tb / t / 1e9 / hbm_peak, "ms": t * 1e3}
+        big = torch.empty(B, 2 * C, 56, 56, device=dev)
+        vd = big[:, 16:16 + C]                # unpack into a channel slice (TMA store path)
+        t = timed(lambda: ctx.unpack(src, vd))
+        assert torch.equal(vd, src)
+        res["unpack_channel_slice_tma"] = {"gbs": 2 * tb / t / 1e9, "frac_hbm": 2 * tb / t / 1e9 / hbm_peak,
+                                           "ms": t * 1e3}
 
     # host-link transfers through the swap engine (per-transfer CUDA events on the copy streams)
     def swap_rates(codec, t_in):

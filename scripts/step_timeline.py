@@ -134,6 +134,8 @@ def main():
         "alloc_wait_ms": st["alloc_wait_ms"] - st0["alloc_wait_ms"], "host_grow_ms": st["host_grow_ms"] - st0["host_grow_ms"],
         "n_host_grow": st["n_host_grow"] - st0["n_host_grow"], "n_scratch_grow": st["n_scratch_grow"] - st0["n_scratch_grow"],
         "pool_driver_ms": st["pool_driver_ms"] - st0["pool_driver_ms"], "n_reclaims": st["n_reclaims"] - st0["n_reclaims"],
+        "unmap_ms": st["unmap_ms"] - st0["unmap_ms"], "map_ms": st["map_ms"] - st0["map_ms"],
+        "access_ms": st["access_ms"] - st0["access_ms"], "n_map": st["n_map"] - st0["n_map"],
         "device_peak_GB": st["device_peak"] / 1e9, "plan_info": ctx.plan_info(),
     }
     print(json.dumps(res, indent=1))

@@ -30,19 +30,36 @@ def _views(dtype):
     yield "scalar", base[0, 0, 0]
     yield "big_rows", (torch.randn(257, 1030, device=dev).to(dtype) if dtype.is_floating_point
                        else torch.randint(0, 5, (257, 1030), device=dev, dtype=dtype))[:, 7:1007]
+    # 16 B-aligned row strides: these take the tensor-map (TMA) path when enabled
+    big = (torch.randn(4, 64, 24, 64, device=dev).to(dtype) if dtype.is_floating_point
+           else torch.randint(-9, 9, (4, 64, 24, 64), device=dev, dtype=dtype))
+    yield "tma_channel_slice", big[:, 8:40]
+    yield "tma_inner_slice", big[:, :, 3:21, 16:48]
+    yield "tma_ragged_box", big[1:, 5:61, :, :48]
+    yield "tma_6d", big.view(4, 8, 8, 24, 8, 8)[:, 1:7, :, 2:22, :, :]
+    wide = (torch.randn(3, 40, 56, 56, device=dev).to(dtype) if dtype.is_floating_point
+            else torch.randint(-9, 9, (3, 40, 56, 56), device=dev, dtype=dtype))
+    yield "tma_odd_box_bytes", wide[:, :, :, 4:52]   # 192 B rows: boxes not a multiple of 128 B
 
 
+@pytest.mark.parametrize("tma", [1, 0])
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_pack_matches_contiguous(lms_ctx, dtype):
-    for name, v in _views(dtype):
-        got = lms_ctx.pack(v)
-        torch.cuda.synchronize()
-        want = v.contiguous()
-        assert torch.equal(got, want), name
+def test_pack_matches_contiguous(lms_ctx, dtype, tma):
+    lms_ctx.set_tuning(0, -1, tma)
+    try:
+        for name, v in _views(dtype):
+            got = lms_ctx.pack(v)
+            torch.cuda.synchronize()
+            want = v.contiguous()
+            assert torch.equal(got, want), name
+    finally:
+        lms_ctx.set_tuning(0, -1, 1)
 
 
+@pytest.mark.parametrize("tma", [1, 0])
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_unpack_matches_copy(lms_ctx, dtype):
+def test_unpack_matches_copy(lms_ctx, dtype, tma):
+    lms_ctx.set_tuning(0, -1, tma)
     for name, v in _views(dtype):
         if name == "expand":
             continue  # overlapping destination: ill-defined scatter
@@ -53,6 +70,7 @@ def test_unpack_matches_copy(lms_ctx, dtype):
         lms_ctx.unpack(src, dst)
         torch.cuda.synchronize()
         assert torch.equal(dst, src), name
+    lms_ctx.set_tuning(0, -1, 1)
 
 
 @pytest.mark.parametrize("bulk", [1, 0])
