@@ -212,6 +212,10 @@ int lms_stats(lms_ctx* ctx, lms_stats_t* out);
 int lms_trace(lms_ctx* ctx, lms_xfer_record_t* out, size_t cap, size_t* n);
 int lms_trace_clear(lms_ctx* ctx);
 int lms_synchronize(lms_ctx* ctx);
+/* Unmap the stale VA aliases page moves leave behind (each cuMemUnmap waits
+ * for the device to drain, so this belongs at a step boundary); returns the
+ * number unmapped via *n (may be NULL). */
+int lms_trim(lms_ctx* ctx, size_t* n);
 
 /* ---- PyTorch CUDAPluggableAllocator hooks (use the global context) -------- */
 void* lms_alloc(size_t size, int device, void* stream);

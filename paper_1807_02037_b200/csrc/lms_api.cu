@@ -469,17 +469,24 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
     return oom(c, size, "live set plus request exceeds the budget");
   if (c->alloc_bytes + rsize > c->limit) reap_until(c, [&] { return c->alloc_bytes + rsize <= c->limit; });
   if (c->alloc_bytes + rsize > c->limit) return oom(c, size, "live set plus request exceeds the budget");
+  // a mapped range first; if freed blocks still wait for their swap-out
+  // copies, wait for those (oldest first: the D2H channel stays busy) before
+  // paying for page moves (driver calls on the host thread)
   std::string err;
-  Block* b = v.alloc(size, stream, false, &err);
-  while (!b && !c->deferred.empty()) {  // fragmented: free the oldest deferred block and retry
+  Block* b = v.alloc(size, stream, false, &err, false);
+  while (!b && !c->deferred.empty()) {
     const size_t before = c->deferred.size();
     reap_until(c, [&] { return c->deferred.size() < before; });
     err.clear();
-    b = v.alloc(size, stream, false, &err);
+    b = v.alloc(size, stream, false, &err, false);
   }
   if (!b) {
     err.clear();
-    b = v.alloc(size, stream, true, &err);
+    b = v.alloc(size, stream, false, &err, true);
+  }
+  if (!b) {
+    err.clear();
+    b = v.alloc(size, stream, true, &err, true);
   }
   if (!b) return oom(c, size, err);
   // a range last used by another stream: wait for that use on the device
@@ -1635,6 +1642,15 @@ int lms_trace_clear(lms_ctx* c) {
   return LMS_OK;
 }
 
+int lms_trim(lms_ctx* c, size_t* n) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  size_t z = c->vmm ? c->vmm->zombies() : 0;
+  if (c->vmm) c->vmm->trim();
+  if (n) *n = z;
+  return LMS_OK;
+}
+
 int lms_synchronize(lms_ctx* c) {
   if (!c) return fail(LMS_E_INVALID, "null ctx");
   CK(cudaStreamSynchronize(c->d2h));
@@ -1642,6 +1658,7 @@ int lms_synchronize(lms_ctx* c) {
   std::lock_guard<std::mutex> g(c->mu);
   reap_deferred(c, false);
   reap_zombies(c);
+  if (c->vmm) c->vmm->trim();
   return LMS_OK;
 }
 

@@ -14,6 +14,13 @@
 // VA range that fits (usually the unmapped tail), so a request that fits the
 // budget never fails for lack of contiguity.
 //
+// A page move does not unmap the page from its old VA: cuMemUnmap waits for
+// the device to drain (measured: 10x spread in host time depending on the
+// queue), so the page is mapped at the new VA as an alias and the old VA
+// page becomes a "zombie" mapping nobody may allocate over.  Zombies are
+// unmapped in bulk by trim() at a quiet point (step end, synchronize), or
+// individually when their VA is needed again (last resort).
+//
 // "Idle" is decided without device-wide synchronisation: every free records
 // an event on the freeing stream and stamps the block with that stream's
 // clock value; a block is idle once its stream's clock has passed the stamp.
@@ -168,6 +175,7 @@ class VmmPool {
     small_.init(base_, small_va_, fresh, Arena::kAlign);
     large_.init(base_ + small_va_, large_va_, fresh, gran_);
     handle_of_.assign((small_va_ + large_va_) / page_, -1);
+    zombie_.assign(handle_of_.size(), -1);
     live_.assign(handle_of_.size(), 0);
     access_.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     access_.location.id = device;
@@ -213,7 +221,8 @@ class VmmPool {
   // Allocate `size` bytes for `stream`.  On success the block is live and
   // backed; *wait_stream/*wait_seq name a stamp the caller's stream must
   // device-wait on (cross-stream reuse of a range not yet idle), or null.
-  Block* alloc(size_t size, void* stream, bool may_block, std::string* err) {
+  // allow_moves=false: only ranges whose pages are all mapped qualify (no driver call)
+  Block* alloc(size_t size, void* stream, bool may_block, std::string* err, bool allow_moves = true) {
     Arena& ar = arena_for(size);
     Block* b = ar.alloc_scored(size, [&](const Block* fb, size_t sz) -> long {
       long unmapped = long(unmapped_in(ar, fb->off, sz));
@@ -222,6 +231,11 @@ class VmmPool {
     });
     if (!b) {
       *err = "VA exhausted";
+      return nullptr;
+    }
+    if (!allow_moves && unmapped_in(ar, b->off, b->size) > 0) {
+      ar.release(b);
+      *err = "no mapped range fits";
       return nullptr;
     }
     pin(b, +1);
@@ -258,6 +272,13 @@ class VmmPool {
   uint64_t n_unmap() const { return n_unmap_; }
   uint64_t n_moves() const { return n_moves_; }
   double driver_ms() const { return driver_s_ * 1e3; }
+  size_t zombies() const { return n_zombie_; }
+  // unmap every zombie alias (call where a device drain costs nothing)
+  void trim() {
+    if (!n_zombie_) return;
+    for (size_t p = 0; p < zombie_.size() && n_zombie_; ++p)
+      if (zombie_[p] >= 0) unmap_zombie(p);
+  }
   double unmap_ms() const { return unmap_s_ * 1e3; }
   double map_ms() const { return map_s_ * 1e3; }
   double access_ms() const { return access_s_ * 1e3; }
@@ -284,7 +305,7 @@ class VmmPool {
   size_t unmapped_in(const Arena& a, size_t off, size_t size) const {
     size_t lo = size_t(a.base() - base_) + off;
     size_t f = lo / page_, l = (lo + a.round_up(size) - 1) / page_, n = 0;
-    for (size_t p = f; p <= l; ++p) n += handle_of_[p] < 0;
+    for (size_t p = f; p <= l; ++p) n += handle_of_[p] < 0 ? (zombie_[p] >= 0 ? 8 : 1) : 0;
     return n;
   }
   void pin(const Block* b, int d) {
@@ -320,24 +341,34 @@ class VmmPool {
         span(fb, &f, &l);
         // only pages the free range owns entirely and no live block touches
         for (size_t p = l + 1; p-- > f && free_.size() < n;) {
-          if (handle_of_[p] >= 0 && live_[p] == 0) unmap_page(p);
+          if (handle_of_[p] >= 0 && live_[p] == 0) retire_page(p);
         }
       }
     }
     return free_.size() >= n;
   }
 
-  void unmap_page(size_t p) {
+  // move-out of a page: its physical handle becomes free for another VA while
+  // the old mapping stays as a zombie (no cuMemUnmap on the hot path)
+  void retire_page(size_t p) {
+    free_.push_back(handle_of_[p]);
+    zombie_[p] = handle_of_[p];
+    handle_of_[p] = -1;
+    --mapped_;
+    ++n_zombie_;
+    ++n_unmap_;
+  }
+
+  void unmap_zombie(size_t p) {
     auto t0 = now();
     drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
     const double dt = secs(t0);
     driver_s_ += dt;
     unmap_s_ += dt;
-    free_.push_back(handle_of_[p]);
-    handle_of_[p] = -1;
-    --mapped_;
-    ++n_unmap_;
+    zombie_[p] = -1;
+    --n_zombie_;
   }
+
 
   bool map_pages(const std::vector<size_t>& pages, std::string* err) {
     auto t0 = now();
@@ -346,6 +377,7 @@ class VmmPool {
       int h = free_.back();
       free_.pop_back();
       size_t p = pages[i];
+      if (zombie_[p] >= 0) unmap_zombie(p);   // its VA is needed again
       auto tm = now();
       const CUresult mr = drv_.map(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_, 0, handles_[h], 0);
       map_s_ += secs(tm);
@@ -379,8 +411,10 @@ class VmmPool {
 
   void teardown() {
     if (!base_) return;
-    for (size_t p = 0; p < handle_of_.size(); ++p)
+    for (size_t p = 0; p < handle_of_.size(); ++p) {
       if (handle_of_[p] >= 0) drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
+      if (zombie_[p] >= 0) drv_.unmap(reinterpret_cast<CUdeviceptr>(base_ + p * page_), page_);
+    }
     for (auto h : handles_) drv_.release(h);
     drv_.address_free(reinterpret_cast<CUdeviceptr>(base_), small_va_ + large_va_);
     base_ = nullptr;
@@ -395,6 +429,8 @@ class VmmPool {
   char* base_ = nullptr;
   Arena small_, large_;
   std::vector<int32_t> handle_of_;   // VA page -> physical page (-1: unmapped)
+  std::vector<int32_t> zombie_;      // VA page -> stale alias of a moved page (-1: none)
+  size_t n_zombie_ = 0;
   std::vector<uint32_t> live_;       // VA page -> live blocks touching it
   std::vector<CUmemGenericAllocationHandle> handles_;
   std::vector<int> free_;            // physical pages not mapped anywhere

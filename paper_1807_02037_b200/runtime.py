@@ -116,6 +116,7 @@ def lib():
         "lms_stats": ([vp, ctypes.POINTER(_Stats)], i),
         "lms_trace": ([vp, ctypes.POINTER(_Xfer), sz, ctypes.POINTER(sz)], i),
         "lms_trace_clear": ([vp], i), "lms_synchronize": ([vp], i),
+        "lms_trim": ([vp, ctypes.POINTER(sz)], i),
         "lms_live_blocks": ([vp, ctypes.POINTER(ctypes.c_uint64), sz, ctypes.POINTER(sz)], i),
     }
     for name, (args, res) in sig.items():
@@ -209,6 +210,12 @@ class Context:
         dev = torch.device("cuda", self.device)
         return (torch.cuda.ExternalStream(a.value, device=dev),
                 torch.cuda.ExternalStream(b.value, device=dev))
+
+    def trim(self) -> int:
+        """Unmap stale VA aliases left by page moves (blocks until the device drains)."""
+        n = ctypes.c_size_t()
+        _check(lib().lms_trim(self.ptr, ctypes.byref(n)), "lms_trim")
+        return n.value
 
     def synchronize(self):
         _check(lib().lms_synchronize(self.ptr), "lms_synchronize")

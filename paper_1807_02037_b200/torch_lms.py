@@ -611,4 +611,7 @@ class LMS:
             except rt.LmsOutOfMemoryError:
                 self.plan_note = "no-fit"   # the placement does not fit: stay dynamic
         self._plan_step += 1
+        # page moves leave stale VA aliases; unmapping them drains the device,
+        # which costs nothing here but would stall the next step's allocator
+        self.ctx.trim()
         return loss
