@@ -154,6 +154,8 @@ typedef struct {
   uint64_t region_bytes, lower_bound_bytes;   /* placement vs max live bytes */
   uint64_t n_items, n_planned;
   uint64_t hits, dynamic, diverged_steps;
+  uint64_t solved_bytes;   /* region the last solve needed (also when it did not fit) */
+  uint64_t room_bytes;     /* budget left for a region next to the live set */
 } lms_plan_info_t;
 int lms_plan_info(lms_ctx* ctx, lms_plan_info_t* out);
 /* the recorded step (after lms_plan_end of a RECORD step): up to `cap` items */

@@ -174,7 +174,7 @@ struct lms_ctx {
     int64_t clock = 0;
     Block* region = nullptr;
     char* base = nullptr;
-    size_t size = 0, lower_bound = 0;
+    size_t size = 0, lower_bound = 0, solved = 0;
     size_t cursor = 0;
     bool diverged = false;
     std::map<size_t, std::pair<size_t, size_t>> live;  // off -> (size, item)
@@ -1171,6 +1171,7 @@ int lms_plan_end(lms_ctx* c) {
   P.rec_held.clear();
   const uint64_t region = plan_place(P.items);
   P.lower_bound = plan_live_peak(P.items);
+  P.solved = region;
   if (region == 0) return LMS_OK;
   // the region is one live block of the dynamic pool; it counts against the budget
   reap_until(c, [&] { return c->alloc_bytes + region <= c->limit; });
@@ -1222,6 +1223,8 @@ int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
   r.ready = P.ready;
   r.region_bytes = P.size;
   r.lower_bound_bytes = P.lower_bound;
+  r.solved_bytes = P.solved;
+  r.room_bytes = c->limit > c->alloc_bytes ? c->limit - c->alloc_bytes + (P.region ? P.size : 0) : 0;
   r.n_items = P.items.size();
   for (auto& it : P.items) r.n_planned += it.planned;
   r.hits = P.hits;

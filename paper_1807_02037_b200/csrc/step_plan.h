@@ -10,8 +10,9 @@
 // (sim.py:116-124, :193-211).
 //
 // Placement is greedy: items in a priority order, each at the lowest offset
-// whose range is free for its whole lifetime.  Two orders are tried (size
-// descending; size x lifetime descending) and the smaller region wins.  No
+// (or in the tightest gap) whose range is free for its whole lifetime.  Three
+// orders (size descending; size x lifetime descending; allocation order) x
+// two gap rules are tried and the smallest region wins.  No
 // CUDA here, so it is unit-testable on the host (lms_plan_solve).
 #pragma once
 
@@ -33,8 +34,10 @@ struct PlanItem {
 
 namespace detail {
 
+// best_fit=false: lowest offset whose gap fits; true: the smallest gap that
+// fits (ties: lowest offset), the region top counting as an unbounded gap
 inline uint64_t place_in_order(std::vector<PlanItem>& it, const std::vector<size_t>& order,
-                               std::vector<uint64_t>* offs) {
+                               std::vector<uint64_t>* offs, bool best_fit = false) {
   offs->assign(it.size(), 0);
   std::vector<size_t> placed;
   placed.reserve(order.size());
@@ -46,9 +49,26 @@ inline uint64_t place_in_order(std::vector<PlanItem>& it, const std::vector<size
       if (it[j].t0 < it[i].t1 && it[i].t0 < it[j].t1) busy.emplace_back((*offs)[j], (*offs)[j] + it[j].size);
     std::sort(busy.begin(), busy.end());
     uint64_t off = 0;
-    for (auto& b : busy) {
-      if (b.first >= off + it[i].size) break;  // the gap before b fits
-      off = std::max(off, b.second);
+    if (!best_fit) {
+      for (auto& b : busy) {
+        if (b.first >= off + it[i].size) break;  // the gap before b fits
+        off = std::max(off, b.second);
+      }
+    } else {
+      uint64_t cur = 0, best_gap = UINT64_MAX;
+      bool found = false;
+      for (auto& b : busy) {
+        if (b.first > cur) {
+          const uint64_t gap = b.first - cur;
+          if (gap >= it[i].size && gap < best_gap) {
+            best_gap = gap;
+            off = cur;
+            found = true;
+          }
+        }
+        cur = std::max(cur, b.second);
+      }
+      if (!found) off = cur;  // above everything live at the same time
     }
     (*offs)[i] = off;
     top = std::max(top, off + it[i].size);
@@ -80,12 +100,20 @@ inline uint64_t plan_place(std::vector<PlanItem>& it) {
     if (aa != bb) return aa > bb;
     return it[a].t0 < it[b].t0;
   });
-  std::vector<uint64_t> o1, o2;
-  const uint64_t s1 = detail::place_in_order(it, by_size, &o1);
-  const uint64_t s2 = detail::place_in_order(it, by_area, &o2);
-  const auto& best = s1 <= s2 ? o1 : o2;
+  auto by_time = idx;  // allocation order (what a dynamic allocator sees)
+  std::vector<std::vector<size_t>*> orders = {&by_size, &by_area, &by_time};
+  uint64_t best_size = UINT64_MAX;
+  std::vector<uint64_t> best, o;
+  for (auto* ord : orders)
+    for (bool bf : {false, true}) {
+      const uint64_t sz = detail::place_in_order(it, *ord, &o, bf);
+      if (sz < best_size) {
+        best_size = sz;
+        best.swap(o);
+      }
+    }
   for (size_t i : idx) it[i].off = best[i];
-  return std::min(s1, s2);
+  return best_size;
 }
 
 // max over time of the bytes live at once: the lower bound any placement

@@ -545,6 +545,7 @@ class LMS:
         # dynamic pool, step 1 is recorded and placed, later steps replay it
         self.static_plan = static_plan
         self._plan_step = 0
+        self._plan_misses = 0
         self.plan_note = None
         self.cfg = cfg
         self.ctx = ctx
@@ -573,11 +574,14 @@ class LMS:
         self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
         return self.plan
 
+    PLAN_ATTEMPTS = 3
+
     def _drop_step_plan(self):
         if self._plan_step >= 2 or self.plan_note == "region":
             torch.cuda.synchronize()
             self.ctx.plan_reset()
         self._plan_step = 0
+        self._plan_misses = 0
         self.plan_note = None
 
     def step(self, x, y):
@@ -596,7 +600,7 @@ class LMS:
             self.optimizer.step()
         except BaseException:
             if mode != rt.PLAN_OFF:
-                self.ctx.plan_end()
+                self.ctx.plan_begin(rt.PLAN_OFF)   # abandon the step's recording/replay
             self.optimizer.zero_grad(set_to_none=True)
             try:
                 self._drop_step_plan()
@@ -609,7 +613,13 @@ class LMS:
                 if mode == rt.PLAN_RECORD:
                     self.plan_note = "region"
             except rt.LmsOutOfMemoryError:
-                self.plan_note = "no-fit"   # the placement does not fit: stay dynamic
+                # the placement does not fit next to the live set: record again
+                # (lifetimes vary with transfer timing), then stay dynamic
+                self._plan_misses += 1
+                if self._plan_misses < self.PLAN_ATTEMPTS:
+                    self._plan_step = 0
+                else:
+                    self.plan_note = "no-fit"
         self._plan_step += 1
         # page moves leave stale VA aliases; unmapping them drains the device,
         # which costs nothing here but would stall the next step's allocator

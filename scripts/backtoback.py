@@ -1,0 +1,81 @@
+"""Back-to-back swapped steps (no host sync between them), as bench.py times them.
+
+Usage: python scripts/backtoback.py --batch 908 --steps 8 [--codec auto] [--e2e]
+Prints per-step device time (CUDA events) and the host-side pool counters per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=908)
+    ap.add_argument("--budget-gib", type=float, default=16.0)
+    ap.add_argument("--codec", default="auto")
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--e2e", action="store_true")
+    ap.add_argument("--no-plan", action="store_true")
+    ap.add_argument("--no-trim", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+    import torchvision
+    from paper_1807_02037_b200 import RewriteConfig, runtime as rt
+    from paper_1807_02037_b200.torch_lms import LMS
+
+    ctx = rt.Context(device=0, device_reserve=int(args.budget_gib * (1 << 30)), host_chunk=4 << 30, timing=True)
+    rt.install_allocator(ctx)
+    torch.backends.cudnn.benchmark = False
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(0)
+    model = torchvision.models.resnet50().to(dev)
+    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
+    lf = torch.nn.functional.cross_entropy
+    lms = LMS(model, lf, opt, RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1), ctx, codec=args.codec,
+              min_swap_bytes=64 << 10, static_plan=not args.no_plan)
+    if args.no_trim:
+        ctx.trim = lambda: 0
+    xc = torch.randn(4, 3, 224, 224, device=dev)
+    yc = torch.randint(0, 1000, (4,), device=dev)
+    lms.capture(xc, yc)
+    del xc, yc
+    x = torch.randn(args.batch, 3, 224, 224, device=dev)
+    y = torch.randint(0, 1000, (args.batch,), device=dev)
+    if args.e2e:
+        xh, yh = x.cpu().pin_memory(), y.cpu().pin_memory()
+        del x, y
+    s = torch.cuda.current_stream()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    keys = ("n_reclaims", "pool_driver_ms", "unmap_ms", "alloc_wait_ms", "n_device_syncs")
+    host = []
+    torch.cuda.synchronize()
+    evs[0].record(s)
+    for i in range(args.steps):
+        st0 = ctx.stats()
+        if args.e2e:
+            xb = xh.to(dev, non_blocking=True)
+            yb = yh.to(dev, non_blocking=True)
+            loss = lms.step(xb, yb)
+            loss.item()
+        else:
+            lms.step(x, y)
+        evs[i + 1].record(s)
+        st1 = ctx.stats()
+        host.append({k: round(st1[k] - st0[k], 1) for k in keys})
+    torch.cuda.synchronize()
+    out = []
+    for i in range(args.steps):
+        out.append({"step": i, "ms": round(evs[i].elapsed_time(evs[i + 1]), 1), **host[i]})
+    print(json.dumps({"args": vars(args), "plan": lms.plan_note, "steps": out}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
