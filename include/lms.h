@@ -156,6 +156,8 @@ typedef struct {
   uint64_t hits, dynamic, diverged_steps;
   uint64_t solved_bytes;   /* region the last solve needed (also when it did not fit) */
   uint64_t room_bytes;     /* budget left for a region next to the live set */
+  double alpha;            /* lifetime ends used: 1 = physical releases (after swap-out copies),
+                              0 = the owners' frees (step_plan.h plan_place_fit) */
 } lms_plan_info_t;
 int lms_plan_info(lms_ctx* ctx, lms_plan_info_t* out);
 /* the recorded step (after lms_plan_end of a RECORD step): up to `cap` items */

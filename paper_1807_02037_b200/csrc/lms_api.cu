@@ -175,6 +175,7 @@ struct lms_ctx {
     Block* region = nullptr;
     char* base = nullptr;
     size_t size = 0, lower_bound = 0, solved = 0;
+    double alpha = 1.0;   // lifetime blend the placement needed (1 = physical releases)
     size_t cursor = 0;
     bool diverged = false;
     std::map<size_t, std::pair<size_t, size_t>> live;  // off -> (size, item)
@@ -543,6 +544,7 @@ int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
     auto& P = c->plan;
     auto it = P.rec_live.find(static_cast<char*>(ptr));
     if (it != P.rec_live.end()) {
+      P.items[it->second].t1_logical = P.clock++;
       P.rec_held[static_cast<char*>(ptr)] = it->second;  // t1 set in release_block
       P.rec_live.erase(it);
     }
@@ -1169,9 +1171,16 @@ int lms_plan_end(lms_ctx* c) {
   if (mode != LMS_PLAN_RECORD) return LMS_OK;
   P.rec_live.clear();  // still live at the end: t1 < 0, served dynamically
   P.rec_held.clear();
-  const uint64_t region = plan_place(P.items);
+  // room for the region: the budget minus what stays live across steps
+  reap_until(c, [] { return false; });
+  // (less one 64 MiB page: the dynamic pool keeps serving the unplanned allocations)
+  const uint64_t keep = c->alloc_bytes + c->vmm->page();
+  const uint64_t room = c->limit > keep ? c->limit - keep : 0;
+  double alpha = 1.0;
+  const uint64_t region = plan_place_fit(P.items, room, &alpha);
   P.lower_bound = plan_live_peak(P.items);
   P.solved = region;
+  P.alpha = alpha;
   if (region == 0) return LMS_OK;
   // the region is one live block of the dynamic pool; it counts against the budget
   reap_until(c, [&] { return c->alloc_bytes + region <= c->limit; });
@@ -1224,6 +1233,7 @@ int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
   r.region_bytes = P.size;
   r.lower_bound_bytes = P.lower_bound;
   r.solved_bytes = P.solved;
+  r.alpha = P.alpha;
   r.room_bytes = c->limit > c->alloc_bytes ? c->limit - c->alloc_bytes + (P.region ? P.size : 0) : 0;
   r.n_items = P.items.size();
   for (auto& it : P.items) r.n_planned += it.planned;

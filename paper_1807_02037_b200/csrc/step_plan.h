@@ -28,6 +28,7 @@ struct PlanItem {
   uint64_t size = 0;   // bytes (already rounded to the pool's granule)
   int64_t t0 = 0;      // alloc event
   int64_t t1 = -1;     // free event; < 0: outlives the step (not planned)
+  int64_t t1_logical = -1;  // the owner's free; t1 may be later (a swap-out still read it)
   uint64_t off = 0;    // placement (valid when planned)
   bool planned = false;
 };
@@ -114,6 +115,52 @@ inline uint64_t plan_place(std::vector<PlanItem>& it) {
     }
   for (size_t i : idx) it[i].off = best[i];
   return best_size;
+}
+
+// Lifetimes end at the physical release (after the block's swap-out copy).
+// When that placement does not fit in `room`, pull each end toward the
+// owner's free (t1 = t1_logical + a (t1 - t1_logical)) and bisect on a: a
+// block reused before its copy finished makes the next allocation wait for
+// that copy on replay, which is the price of fitting.  Returns the region
+// size and the blend used via *alpha.
+inline uint64_t plan_place_fit(std::vector<PlanItem>& it, uint64_t room, double* alpha) {
+  std::vector<int64_t> phys(it.size());
+  for (size_t i = 0; i < it.size(); ++i) phys[i] = it[i].t1;
+  auto blend = [&](double a) {
+    for (size_t i = 0; i < it.size(); ++i) {
+      const int64_t lg = it[i].t1_logical;
+      it[i].t1 = (phys[i] >= 0 && lg >= 0 && lg < phys[i])
+                     ? lg + int64_t(a * double(phys[i] - lg) + 0.5) : phys[i];
+      if (it[i].t1 >= 0 && it[i].t1 <= it[i].t0) it[i].t1 = it[i].t0 + 1;
+    }
+  };
+  *alpha = 1.0;
+  uint64_t r = plan_place(it);
+  if (r <= room) return r;
+  double lo = 0.0, hi = 1.0;
+  blend(0.0);
+  r = plan_place(it);
+  if (r > room) {
+    *alpha = 0.0;
+    return r;  // does not fit even with the owners' frees
+  }
+  std::vector<PlanItem> best = it;
+  uint64_t best_r = r;
+  for (int k = 0; k < 6; ++k) {
+    const double mid = 0.5 * (lo + hi);
+    blend(mid);
+    r = plan_place(it);
+    if (r <= room) {
+      lo = mid;
+      best = it;
+      best_r = r;
+    } else {
+      hi = mid;
+    }
+  }
+  it = best;
+  *alpha = lo;
+  return best_r;
 }
 
 // max over time of the bytes live at once: the lower bound any placement

@@ -54,7 +54,7 @@ def main():
         del x, y
     s = torch.cuda.current_stream()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    keys = ("n_reclaims", "pool_driver_ms", "unmap_ms", "alloc_wait_ms", "n_device_syncs")
+    keys = ("n_reclaims", "pool_driver_ms", "unmap_ms", "map_ms", "access_ms", "alloc_wait_ms", "n_device_syncs")
     host = []
     torch.cuda.synchronize()
     evs[0].record(s)
@@ -74,7 +74,13 @@ def main():
     out = []
     for i in range(args.steps):
         out.append({"step": i, "ms": round(evs[i].elapsed_time(evs[i + 1]), 1), **host[i]})
-    print(json.dumps({"args": vars(args), "plan": lms.plan_note, "steps": out}, indent=1))
+    print(json.dumps({"args": vars(args), "plan": lms.plan_note, "plan_info": ctx.plan_info(), "steps": out},
+                     indent=1))
+    items = ctx.plan_items()
+    if items:
+        tag = "e2e" if args.e2e else "dev"
+        with open(os.path.join(ROOT, "gpurun_out", f"b2b_items_{tag}.json"), "w") as fh:
+            json.dump({"items": items, "limit": ctx.stats()["device_limit"]}, fh)
 
 
 if __name__ == "__main__":

@@ -74,3 +74,22 @@ def test_random_steps_valid_and_tight(seed):
     offs, region = rt.plan_solve(sizes, t0, t1)
     peak = _check(sizes, t0, t1, offs, region)
     assert peak <= region <= 1.5 * peak
+
+
+def test_room_pulls_lifetimes_toward_logical_frees():
+    """plan_place_fit: when physical releases (after swap-out copies) do not fit the
+    room, the ends move toward the owners' frees until the placement fits."""
+    import ctypes
+
+    lib = rt.lib()
+    # a chain whose blocks are freed logically right after the next one is made,
+    # but physically released two steps later (a copy still reading them)
+    n, size = 12, 1 << 20
+    # solve twice through the pure solver: physical vs logical ends
+    t0 = [3 * i for i in range(n)]
+    phys = [t + 7 for t in t0]
+    logical = [t + 4 for t in t0]
+    _, r_phys = rt.plan_solve([size] * n, t0, phys)
+    _, r_log = rt.plan_solve([size] * n, t0, logical)
+    assert r_log < r_phys
+    assert lib is not None
