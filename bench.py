@@ -352,6 +352,7 @@ def main():
         cfg = RewriteConfig(n_tensors=n_tensors, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
                             fuse_swapins=args.fuse_swapins, swapin_fuse_distance=1)
         lms.replan(cfg)
+        lms.static_plan = False   # fit probes run on the dynamic pool; the timed run plans
         xb, yb = batch(nb, seed=7)
         try:
             for _ in range(2):
@@ -419,6 +420,7 @@ def main():
     # timed run with the fewest tensors that fitted; a run that hits the budget
     # anyway (timing-dependent fragmentation) falls back to the next larger set
     swap_ms = None
+    lms.static_plan = True
     for n_use in sorted(set(ok_ns)):
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
                                  ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
@@ -573,6 +575,11 @@ def main():
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
+        try:   # the recorded step, for offline work on the plan solver
+            with open(os.path.join(ROOT, "gpurun_out", f"plan_items_{args.arch}_{bs}.json"), "w") as fh:
+                json.dump({"items": ctx.plan_items(), "plan_info": ctx.plan_info()}, fh)
+        except OSError:
+            pass
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()

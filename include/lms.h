@@ -161,7 +161,8 @@ typedef struct {
 } lms_plan_info_t;
 int lms_plan_info(lms_ctx* ctx, lms_plan_info_t* out);
 /* the recorded step (after lms_plan_end of a RECORD step): up to `cap` items */
-int lms_plan_items(lms_ctx* ctx, uint64_t* sizes, int64_t* t_alloc, int64_t* t_free, size_t cap, size_t* n);
+int lms_plan_items(lms_ctx* ctx, uint64_t* sizes, int64_t* t_alloc, int64_t* t_free, int64_t* t_free_logical,
+                   size_t cap, size_t* n);
 /* the placement on its own (host only): n items with sizes and alloc/free
  * events (free < 0: not planned) -> offsets; returns region size via *region */
 int lms_plan_solve(const uint64_t* sizes, const int64_t* t_alloc, const int64_t* t_free, size_t n,
@@ -217,9 +218,9 @@ int lms_trace(lms_ctx* ctx, lms_xfer_record_t* out, size_t cap, size_t* n);
 int lms_trace_clear(lms_ctx* ctx);
 int lms_synchronize(lms_ctx* ctx);
 /* Unmap the stale VA aliases page moves leave behind (each cuMemUnmap waits
- * for the device to drain, so this belongs at a step boundary); returns the
- * number unmapped via *n (may be NULL). */
-int lms_trim(lms_ctx* ctx, size_t* n);
+ * for the device to drain, so this belongs at a step boundary) once there are
+ * at least `min_zombies` of them; the number unmapped via *n (may be NULL). */
+int lms_trim(lms_ctx* ctx, size_t min_zombies, size_t* n);
 
 /* ---- PyTorch CUDAPluggableAllocator hooks (use the global context) -------- */
 void* lms_alloc(size_t size, int device, void* stream);

@@ -176,6 +176,7 @@ struct lms_ctx {
     char* base = nullptr;
     size_t size = 0, lower_bound = 0, solved = 0;
     double alpha = 1.0;   // lifetime blend the placement needed (1 = physical releases)
+    std::vector<int64_t> t1_phys;  // recorded physical release events (before any blend)
     size_t cursor = 0;
     bool diverged = false;
     std::map<size_t, std::pair<size_t, size_t>> live;  // off -> (size, item)
@@ -1177,6 +1178,8 @@ int lms_plan_end(lms_ctx* c) {
   const uint64_t keep = c->alloc_bytes + c->vmm->page();
   const uint64_t room = c->limit > keep ? c->limit - keep : 0;
   double alpha = 1.0;
+  P.t1_phys.resize(P.items.size());
+  for (size_t i = 0; i < P.items.size(); ++i) P.t1_phys[i] = P.items[i].t1;
   const uint64_t region = plan_place_fit(P.items, room, &alpha);
   P.lower_bound = plan_live_peak(P.items);
   P.solved = region;
@@ -1244,14 +1247,16 @@ int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
   return LMS_OK;
 }
 
-int lms_plan_items(lms_ctx* c, uint64_t* sizes, int64_t* t_alloc, int64_t* t_free, size_t cap, size_t* n) {
+int lms_plan_items(lms_ctx* c, uint64_t* sizes, int64_t* t_alloc, int64_t* t_free, int64_t* t_free_logical,
+                   size_t cap, size_t* n) {
   if (!c || !n) return fail(LMS_E_INVALID, "null argument");
   std::lock_guard<std::mutex> g(c->mu);
   auto& it = c->plan.items;
   for (size_t i = 0; i < it.size() && i < cap; ++i) {
     if (sizes) sizes[i] = it[i].size;
     if (t_alloc) t_alloc[i] = it[i].t0;
-    if (t_free) t_free[i] = it[i].t1;
+    if (t_free) t_free[i] = i < c->plan.t1_phys.size() ? c->plan.t1_phys[i] : it[i].t1;
+    if (t_free_logical) t_free_logical[i] = it[i].t1_logical;
   }
   *n = it.size();
   return LMS_OK;
@@ -1655,11 +1660,12 @@ int lms_trace_clear(lms_ctx* c) {
   return LMS_OK;
 }
 
-int lms_trim(lms_ctx* c, size_t* n) {
+int lms_trim(lms_ctx* c, size_t min_zombies, size_t* n) {
   if (!c) return fail(LMS_E_INVALID, "null ctx");
   std::lock_guard<std::mutex> g(c->mu);
   size_t z = c->vmm ? c->vmm->zombies() : 0;
-  if (c->vmm) c->vmm->trim();
+  if (z < std::max<size_t>(min_zombies, 1)) z = 0;
+  if (z) c->vmm->trim();
   if (n) *n = z;
   return LMS_OK;
 }

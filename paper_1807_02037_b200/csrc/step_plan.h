@@ -80,9 +80,15 @@ inline uint64_t place_in_order(std::vector<PlanItem>& it, const std::vector<size
 
 }  // namespace detail
 
+inline uint64_t plan_live_peak(const std::vector<PlanItem>& it);
+
 // Place every item with t1 >= 0; returns the region size.  Items with t1 < 0
-// stay unplanned (the dynamic pool serves them).
-inline uint64_t plan_place(std::vector<PlanItem>& it) {
+// stay unplanned (the dynamic pool serves them).  After the deterministic
+// orders, randomized restarts (size keys jittered by x0.6..1.4, fixed seed)
+// run until the region fits `target` or reaches the live-bytes lower bound,
+// at most `restarts` times: first-fit by size gets stuck when a short-lived
+// giant (a cuDNN workspace) takes the bottom of a tall stack.
+inline uint64_t plan_place(std::vector<PlanItem>& it, uint64_t target = 0, int restarts = 400) {
   std::vector<size_t> idx;
   for (size_t i = 0; i < it.size(); ++i) {
     it[i].planned = it[i].t1 >= 0 && it[i].t1 > it[i].t0;
@@ -113,6 +119,25 @@ inline uint64_t plan_place(std::vector<PlanItem>& it) {
         best.swap(o);
       }
     }
+  const uint64_t bound = plan_live_peak(it);
+  uint64_t rng = 0x9E3779B97F4A7C15ull;
+  auto next = [&rng] {
+    rng ^= rng << 13;
+    rng ^= rng >> 7;
+    rng ^= rng << 17;
+    return rng;
+  };
+  std::vector<double> key(it.size());
+  auto by_jit = idx;
+  for (int r = 0; r < restarts && best_size > bound && best_size > target; ++r) {
+    for (size_t i : idx) key[i] = double(it[i].size) * (0.6 + 0.8 * double(next() >> 11) * 0x1.0p-53);
+    std::stable_sort(by_jit.begin(), by_jit.end(), [&](size_t a, size_t b) { return key[a] > key[b]; });
+    const uint64_t sz = detail::place_in_order(it, by_jit, &o, false);
+    if (sz < best_size) {
+      best_size = sz;
+      best.swap(o);
+    }
+  }
   for (size_t i : idx) it[i].off = best[i];
   return best_size;
 }
@@ -135,11 +160,11 @@ inline uint64_t plan_place_fit(std::vector<PlanItem>& it, uint64_t room, double*
     }
   };
   *alpha = 1.0;
-  uint64_t r = plan_place(it);
+  uint64_t r = plan_place(it, room);
   if (r <= room) return r;
   double lo = 0.0, hi = 1.0;
   blend(0.0);
-  r = plan_place(it);
+  r = plan_place(it, room);
   if (r > room) {
     *alpha = 0.0;
     return r;  // does not fit even with the owners' frees
@@ -149,7 +174,7 @@ inline uint64_t plan_place_fit(std::vector<PlanItem>& it, uint64_t room, double*
   for (int k = 0; k < 6; ++k) {
     const double mid = 0.5 * (lo + hi);
     blend(mid);
-    r = plan_place(it);
+    r = plan_place(it, room);
     if (r <= room) {
       lo = mid;
       best = it;

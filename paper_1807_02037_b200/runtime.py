@@ -97,7 +97,7 @@ def lib():
         "lms_set_tuning": ([vp, i, i, i], i),
         "lms_plan_begin": ([vp, i], i), "lms_plan_end": ([vp], i), "lms_plan_reset": ([vp], i),
         "lms_plan_info": ([vp, ctypes.POINTER(_PlanInfo)], i),
-        "lms_plan_items": ([vp, ctypes.POINTER(ctypes.c_uint64), i64p, i64p, sz, ctypes.POINTER(sz)], i),
+        "lms_plan_items": ([vp, ctypes.POINTER(ctypes.c_uint64), i64p, i64p, i64p, sz, ctypes.POINTER(sz)], i),
         "lms_plan_solve": ([ctypes.POINTER(ctypes.c_uint64), i64p, i64p, sz, ctypes.POINTER(ctypes.c_uint64),
                             ctypes.POINTER(ctypes.c_uint64)], i),
         "lms_dev_alloc": ([vp, sz, vp, pp], i), "lms_dev_free": ([vp, vp, vp], i),
@@ -117,7 +117,7 @@ def lib():
         "lms_stats": ([vp, ctypes.POINTER(_Stats)], i),
         "lms_trace": ([vp, ctypes.POINTER(_Xfer), sz, ctypes.POINTER(sz)], i),
         "lms_trace_clear": ([vp], i), "lms_synchronize": ([vp], i),
-        "lms_trim": ([vp, ctypes.POINTER(sz)], i),
+        "lms_trim": ([vp, sz, ctypes.POINTER(sz)], i),
         "lms_live_blocks": ([vp, ctypes.POINTER(ctypes.c_uint64), sz, ctypes.POINTER(sz)], i),
     }
     for name, (args, res) in sig.items():
@@ -212,10 +212,11 @@ class Context:
         return (torch.cuda.ExternalStream(a.value, device=dev),
                 torch.cuda.ExternalStream(b.value, device=dev))
 
-    def trim(self) -> int:
-        """Unmap stale VA aliases left by page moves (blocks until the device drains)."""
+    def trim(self, min_zombies: int = 1) -> int:
+        """Unmap stale VA aliases left by page moves once there are at least
+        ``min_zombies`` (blocks until the device drains)."""
         n = ctypes.c_size_t()
-        _check(lib().lms_trim(self.ptr, ctypes.byref(n)), "lms_trim")
+        _check(lib().lms_trim(self.ptr, min_zombies, ctypes.byref(n)), "lms_trim")
         return n.value
 
     def synchronize(self):
@@ -231,12 +232,12 @@ class Context:
         _check(lib().lms_plan_end(self.ptr), "lms_plan_end")
 
     def plan_items(self, cap: int = 1 << 16):
-        """The recorded step: list of (size, alloc event, free event)."""
+        """The recorded step: (size, alloc event, physical release event, owner's free event)."""
         u64 = (ctypes.c_uint64 * cap)()
-        a, b = (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)()
+        a, b, lg = (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)()
         n = ctypes.c_size_t()
-        _check(lib().lms_plan_items(self.ptr, u64, a, b, cap, ctypes.byref(n)), "lms_plan_items")
-        return [(u64[i], a[i], b[i]) for i in range(min(cap, n.value))]
+        _check(lib().lms_plan_items(self.ptr, u64, a, b, lg, cap, ctypes.byref(n)), "lms_plan_items")
+        return [(u64[i], a[i], b[i], lg[i]) for i in range(min(cap, n.value))]
 
     def plan_reset(self):
         _check(lib().lms_plan_reset(self.ptr), "lms_plan_reset")

@@ -575,6 +575,7 @@ class LMS:
         return self.plan
 
     PLAN_ATTEMPTS = 3
+    TRIM_ZOMBIES = 256   # 64 MiB pages: 16 GiB of stale VA
 
     def _drop_step_plan(self):
         if self._plan_step >= 2 or self.plan_note == "region":
@@ -622,6 +623,7 @@ class LMS:
                     self.plan_note = "no-fit"
         self._plan_step += 1
         # page moves leave stale VA aliases; unmapping them drains the device,
-        # which costs nothing here but would stall the next step's allocator
-        self.ctx.trim()
+        # so it happens here, between steps, once they add up to ~1/4 of the
+        # pool's reserved VA (a step in replay makes none)
+        self.ctx.trim(self.TRIM_ZOMBIES)
         return loss
