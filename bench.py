@@ -434,7 +434,7 @@ def main():
             st0 = ctx.stats()
             clocks = Clocks(local)
             clocks.start()
-            swap_ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps)
+            swap_ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps, tag="swapped")
             clk = clocks.stop()
             break
         except RuntimeError as e:
@@ -469,7 +469,7 @@ def main():
         return loss.item()
 
     e2e_step()
-    e2e_ms = timed(torch, dev, ws, e2e_step, args.steps)
+    e2e_ms = timed(torch, dev, ws, e2e_step, args.steps, tag="e2e")
     e2e_val = bs * ws * args.steps / (e2e_ms * 1e-3)
 
     # ---- 6. link peak, CPU baseline -----------------------------------------
@@ -571,6 +571,7 @@ def main():
         "e2e": {"value": round(e2e_val, 2), "unit": unit_name(args), "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": kernels,
+        "step_ms": STEP_MS,
         "clocks": clk,
     }
     if rank == 0:
@@ -597,18 +598,24 @@ def metric_name(args) -> str:
             f"under an enforced {args.budget_gib:g} GiB per-GPU budget ({what}, TFLMS swapping)")
 
 
-def timed(torch, dev, ws, fn, steps):
+STEP_MS = {}
+
+
+def timed(torch, dev, ws, fn, steps, tag=None):
     """Device time of exactly ``steps`` calls: barrier + sync on both sides, max over ranks."""
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    e0, e1 = evs[0], evs[-1]
     e0.record()
-    for _ in range(steps):
+    for k in range(steps):
         fn()
-    e1.record()
+        evs[k + 1].record()
     torch.cuda.synchronize(dev)
+    if tag:
+        STEP_MS[tag] = [round(evs[k].elapsed_time(evs[k + 1]), 1) for k in range(steps)]
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -1174,9 +1174,10 @@ int lms_plan_end(lms_ctx* c) {
   P.rec_held.clear();
   // room for the region: the budget minus what stays live across steps
   reap_until(c, [] { return false; });
-  // (less one 64 MiB page: the dynamic pool keeps serving the unplanned allocations)
-  const uint64_t keep = c->alloc_bytes + c->vmm->page();
-  const uint64_t room = c->limit > keep ? c->limit - keep : 0;
+  // in whole physical pages: those no live block touches (the region needs its
+  // own pages), less one page for the dynamic pool's unplanned allocations
+  const size_t free_pages = c->vmm->limit_pages() - std::min(c->vmm->limit_pages(), c->vmm->live_pages());
+  const uint64_t room = free_pages > 1 ? uint64_t(free_pages - 1) * c->vmm->page() : 0;
   double alpha = 1.0;
   P.t1_phys.resize(P.items.size());
   for (size_t i = 0; i < P.items.size(); ++i) P.t1_phys[i] = P.items[i].t1;
@@ -1237,7 +1238,10 @@ int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
   r.lower_bound_bytes = P.lower_bound;
   r.solved_bytes = P.solved;
   r.alpha = P.alpha;
-  r.room_bytes = c->limit > c->alloc_bytes ? c->limit - c->alloc_bytes + (P.region ? P.size : 0) : 0;
+  {
+    const size_t lp = c->vmm ? c->vmm->live_pages() : 0, tp = c->vmm ? c->vmm->limit_pages() : 0;
+    r.room_bytes = tp > lp ? uint64_t(tp - lp) * c->vmm->page() + (P.region ? P.size : 0) : 0;
+  }
   r.n_items = P.items.size();
   for (auto& it : P.items) r.n_planned += it.planned;
   r.hits = P.hits;

@@ -267,6 +267,7 @@ class VmmPool {
 
   size_t live_bytes() const { return bytes_live_; }
   size_t live_pages() const { return live_pages_; }
+  size_t limit_pages() const { return limit_pages_; }
   size_t mapped_bytes() const { return mapped_ * page_; }
   uint64_t n_map() const { return n_map_; }
   uint64_t n_unmap() const { return n_unmap_; }
