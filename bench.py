@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--fuse-swapins", action="store_true", default=True)
     ap.add_argument("--no-fuse-swapins", dest="fuse_swapins", action="store_false")
     ap.add_argument("--b0", type=int, default=0, help="skip bisection and use this no-swap batch")
-    ap.add_argument("--n-tensors", type=int, default=-1,
-                    help="swap only the first n candidate tensors (rewrite BFS order); -1 = all")
+    ap.add_argument("--n-tensors", type=int, default=0,
+                    help="swap only the first n candidate tensors (rewrite BFS order); -1 = all; "
+                         "0 = try all but the last 1/12 (the shortest-lived), else all")
     ap.add_argument("--search", type=int, default=0,
                     help="probes of the n_tensors bisection (0: swap every candidate tensor)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
@@ -386,8 +387,9 @@ def main():
     # then bisect on n_tensors starting from the estimate
     N = len(order)
     ok_ns = []
-    if 0 < args.n_tensors < N and try_swap(bs, args.n_tensors):
-        ok_ns.append(args.n_tensors)
+    n_first = args.n_tensors if args.n_tensors else N - max(1, N // 12)
+    if 0 < n_first < N and try_swap(bs, n_first):
+        ok_ns.append(n_first)
     fitted = try_swap(bs, -1)
     if fitted:
         ok_ns.append(N)
