@@ -142,7 +142,10 @@ int lms_handle_layout(lms_handle* h, int64_t* strides_out, int64_t* storage_elem
  * recorded offsets: no fragmentation, no page moves; a step that allocates
  * differently falls back to the dynamic pool from the first mismatch on.
  * Residency intervals are the reference's model, sim.py:116-124, :193-211. */
-enum { LMS_PLAN_OFF = 0, LMS_PLAN_RECORD = 1, LMS_PLAN_REPLAY = 2 };
+/* REFINE replays like REPLAY and also observes when each planned block's
+ * swap-out copy finished; lms_plan_end then re-places the step with those
+ * (replay-speed) lifetimes and adopts the result if it fits the region. */
+enum { LMS_PLAN_OFF = 0, LMS_PLAN_RECORD = 1, LMS_PLAN_REPLAY = 2, LMS_PLAN_REFINE = 3 };
 int lms_plan_begin(lms_ctx* ctx, int mode);
 /* ends the step; after RECORD it solves the placement and reserves the
  * region (LMS_E_OOM if the region does not fit the budget: no plan) */
@@ -158,6 +161,7 @@ typedef struct {
   uint64_t room_bytes;     /* budget left for a region next to the live set */
   double alpha;            /* lifetime ends used: 1 = physical releases (after swap-out copies),
                               0 = the owners' frees (step_plan.h plan_place_fit) */
+  uint64_t refinements;    /* REFINE steps whose re-placement was adopted */
 } lms_plan_info_t;
 int lms_plan_info(lms_ctx* ctx, lms_plan_info_t* out);
 /* the recorded step (after lms_plan_end of a RECORD step): up to `cap` items */

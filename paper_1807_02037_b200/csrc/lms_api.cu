@@ -164,6 +164,8 @@ struct lms_ctx {
     void* stream;
     uint64_t seq;
     char* base;   // key of the block's swap-out holds
+    size_t item;  // plan item it served
+    bool released;  // its swap-out copies were seen finished
   };
   struct StepPlan {
     int mode = LMS_PLAN_OFF;
@@ -177,6 +179,9 @@ struct lms_ctx {
     size_t size = 0, lower_bound = 0, solved = 0;
     double alpha = 1.0;   // lifetime blend the placement needed (1 = physical releases)
     std::vector<int64_t> t1_phys;  // recorded physical release events (before any blend)
+    std::vector<PlanItem> refine;  // REFINE: lifetimes observed while replaying
+    int64_t rclock = 0;
+    uint64_t refinements = 0;
     size_t cursor = 0;
     bool diverged = false;
     std::map<size_t, std::pair<size_t, size_t>> live;  // off -> (size, item)
@@ -408,8 +413,13 @@ int plan_alloc(lms_ctx* c, size_t rsize, void* stream, void** out) {
   const auto t0 = std::chrono::steady_clock::now();
   bool waited = false;
   size_t w = 0;
+  const bool refine = P.mode == LMS_PLAN_REFINE;
   for (size_t i = 0; i < P.freed.size(); ++i) {
-    lms_ctx::PlanFreed f = P.freed[i];
+    lms_ctx::PlanFreed& f = P.freed[i];
+    if (refine && !f.released && holds_clear(c, f.base)) {
+      f.released = true;  // seen released before this allocation
+      P.refine[f.item].t1 = P.rclock;
+    }
     const bool overlap = f.off < hi && lo < f.off + f.size;
     if (overlap) {
       if (!holds_clear(c, f.base)) {
@@ -421,10 +431,17 @@ int plan_alloc(lms_ctx* c, size_t rsize, void* stream, void** out) {
         c->st.n_cross_stream_waits++;
       }
     }
-    // keep entries whose range may still be busy for some later request
-    if (!(holds_clear(c, f.base) && c->vmm->clocks_.passed(f.stream, f.seq))) P.freed[w++] = f;
+    if (refine && !f.released && holds_clear(c, f.base)) {
+      f.released = true;  // this allocation waited for it
+      P.refine[f.item].t1 = P.rclock;
+    }
+    // keep entries whose range may still be busy for some later request (and,
+    // when refining, whose release has not been seen yet)
+    if (!(holds_clear(c, f.base) && c->vmm->clocks_.passed(f.stream, f.seq)) || (refine && !f.released))
+      P.freed[w++] = f;
   }
   P.freed.resize(w);
+  if (refine) P.refine[idx].t0 = P.rclock++;
   if (waited)
     c->st.alloc_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   P.live[lo] = {it.size, idx};
@@ -442,9 +459,16 @@ void plan_free(lms_ctx* c, void* ptr, void* stream) {
   auto it = P.live.find(off);
   if (it == P.live.end()) return;
   const size_t size = it->second.first;
+  const size_t item = it->second.second;
   P.live.erase(it);
   P.live_bytes -= size;
-  P.freed.push_back({off, size, stream, c->vmm->clocks_.stamp(stream), static_cast<char*>(ptr)});
+  bool released = true;
+  if (P.mode == LMS_PLAN_REFINE) {
+    P.refine[item].t1_logical = P.rclock++;
+    released = holds_clear(c, static_cast<char*>(ptr));
+    if (released) P.refine[item].t1 = P.refine[item].t1_logical;
+  }
+  P.freed.push_back({off, size, stream, c->vmm->clocks_.stamp(stream), static_cast<char*>(ptr), item, released});
   c->st.n_free++;
 }
 
@@ -458,11 +482,12 @@ int dev_alloc_locked(lms_ctx* c, size_t size, void* stream, void** out) {
   VmmPool& v = *c->vmm;
   reap_deferred(c, false);
   const size_t rsize = Arena::round(size);
-  if (c->plan.mode == LMS_PLAN_REPLAY && c->plan.ready && !c->plan.diverged) {
+  const bool replaying = c->plan.mode == LMS_PLAN_REPLAY || c->plan.mode == LMS_PLAN_REFINE;
+  if (replaying && c->plan.ready && !c->plan.diverged) {
     rc = plan_alloc(c, rsize, stream, out);
     if (rc == LMS_OK) return LMS_OK;
   }
-  if (c->plan.mode == LMS_PLAN_REPLAY) c->plan.dynamic++;
+  if (replaying) c->plan.dynamic++;
   // the budget is on live bytes; the non-deferred live set only shrinks by
   // frees the caller has not made yet, so fail at once if it plus the request
   // is over (cuDNN's plan loop probes oversized workspaces and expects a
@@ -1141,7 +1166,7 @@ int lms_dev_hold_until(lms_ctx* c, const void* ptr, void* stream) {
 
 int lms_plan_begin(lms_ctx* c, int mode) {
   if (!c) return fail(LMS_E_INVALID, "null ctx");
-  if (mode != LMS_PLAN_RECORD && mode != LMS_PLAN_REPLAY && mode != LMS_PLAN_OFF)
+  if (mode != LMS_PLAN_RECORD && mode != LMS_PLAN_REPLAY && mode != LMS_PLAN_REFINE && mode != LMS_PLAN_OFF)
     return fail(LMS_E_INVALID, "bad plan mode");
   std::lock_guard<std::mutex> g(c->mu);
   int rc = ensure_pool(c);
@@ -1154,10 +1179,16 @@ int lms_plan_begin(lms_ctx* c, int mode) {
     P.rec_held.clear();
     P.clock = 0;
     P.ready = false;
-  } else if (mode == LMS_PLAN_REPLAY) {
+  } else if (mode == LMS_PLAN_REPLAY || mode == LMS_PLAN_REFINE) {
     if (!P.ready) return fail(LMS_E_STATE, "no recorded plan");
     P.cursor = 0;
     P.diverged = false;
+    if (mode == LMS_PLAN_REFINE) {
+      P.refine = P.items;
+      for (auto& x : P.refine) x.t0 = 0, x.t1 = -1, x.t1_logical = -1;
+      P.rclock = 0;
+      for (auto& f : P.freed) f.released = true;  // the previous step's frees are not this step's
+    }
   }
   P.mode = mode;
   return LMS_OK;
@@ -1169,6 +1200,33 @@ int lms_plan_end(lms_ctx* c) {
   auto& P = c->plan;
   const int mode = P.mode;
   P.mode = LMS_PLAN_OFF;
+  if (mode == LMS_PLAN_REFINE) {
+    // re-place with the lifetimes this replay step showed; adopt the new
+    // placement only if it fits the region already held
+    if (P.diverged || !P.live.empty()) return LMS_OK;
+    std::vector<PlanItem> nx = P.refine;
+    for (size_t i = 0; i < nx.size(); ++i) {
+      if (!P.items[i].planned) {
+        nx[i].t1 = -1;  // served dynamically: stays so
+        continue;
+      }
+      if (nx[i].t1 < 0) nx[i].t1 = P.rclock + 1;  // copy not seen finished within the step
+      if (nx[i].t1_logical < 0) nx[i].t1_logical = nx[i].t1;
+    }
+    double alpha = 1.0;
+    const uint64_t region = plan_place_fit(nx, P.size, &alpha);
+    if (region <= P.size) {
+      for (size_t f = 0; f < P.freed.size(); ++f) drain_holds(c, P.freed[f].base);
+      CK(cudaDeviceSynchronize());   // old placement's users finished
+      P.freed.clear();
+      P.items.swap(nx);
+      P.solved = region;
+      P.alpha = alpha;
+      P.lower_bound = plan_live_peak(P.items);
+      P.refinements++;
+    }
+    return LMS_OK;
+  }
   if (mode != LMS_PLAN_RECORD) return LMS_OK;
   P.rec_live.clear();  // still live at the end: t1 < 0, served dynamically
   P.rec_held.clear();
@@ -1238,6 +1296,7 @@ int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
   r.lower_bound_bytes = P.lower_bound;
   r.solved_bytes = P.solved;
   r.alpha = P.alpha;
+  r.refinements = P.refinements;
   {
     const size_t lp = c->vmm ? c->vmm->live_pages() : 0, tp = c->vmm ? c->vmm->limit_pages() : 0;
     r.room_bytes = tp > lp ? uint64_t(tp - lp) * c->vmm->page() + (P.region ? P.size : 0) : 0;

@@ -68,10 +68,10 @@ class _PlanInfo(ctypes.Structure):
                 ("lower_bound_bytes", ctypes.c_uint64), ("n_items", ctypes.c_uint64),
                 ("n_planned", ctypes.c_uint64), ("hits", ctypes.c_uint64), ("dynamic", ctypes.c_uint64),
                 ("diverged_steps", ctypes.c_uint64), ("solved_bytes", ctypes.c_uint64),
-                ("room_bytes", ctypes.c_uint64), ("alpha", ctypes.c_double)]
+                ("room_bytes", ctypes.c_uint64), ("alpha", ctypes.c_double), ("refinements", ctypes.c_uint64)]
 
 
-PLAN_OFF, PLAN_RECORD, PLAN_REPLAY = 0, 1, 2
+PLAN_OFF, PLAN_RECORD, PLAN_REPLAY, PLAN_REFINE = 0, 1, 2, 3
 
 _lib = None
 

@@ -575,6 +575,9 @@ class LMS:
         return self.plan
 
     PLAN_ATTEMPTS = 3
+    # replay steps that re-place the plan with the lifetimes they observe (the
+    # recorded step ran on the dynamic pool and is slower than a replay)
+    REFINE_STEPS = (2,)
     TRIM_ZOMBIES = 256   # 64 MiB pages: 16 GiB of stale VA
 
     def _drop_step_plan(self):
@@ -589,7 +592,9 @@ class LMS:
         """One swapped training step; returns the loss tensor (on device)."""
         mode = rt.PLAN_OFF
         if self.static_plan and self.plan_note != "no-fit":
-            mode = rt.PLAN_RECORD if self._plan_step == 1 else rt.PLAN_REPLAY if self._plan_step >= 2 else rt.PLAN_OFF
+            mode = (rt.PLAN_RECORD if self._plan_step == 1
+                    else rt.PLAN_REFINE if self._plan_step in self.REFINE_STEPS and self.plan_note == "region"
+                    else rt.PLAN_REPLAY if self._plan_step >= 2 else rt.PLAN_OFF)
         if mode == rt.PLAN_RECORD:
             torch.cuda.synchronize()
             self.ctx.plan_reset()       # a plan left over from a failed step
