@@ -62,6 +62,8 @@ def parse():
                     help="probes of the n_tensors bisection (0: swap every candidate tensor)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--tf32", action="store_true")
+    ap.add_argument("--ddp", action="store_true",
+                    help="wrap the model in DistributedDataParallel even at one rank (exercises the DP path)")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
     return ap.parse_args()
 
@@ -189,8 +191,11 @@ def main():
     # the link's copy-engine peak, measured first while the pool is empty
     link = measure_host_link(torch, dev)
     gc.collect()
-    if ws > 1:
+    use_dist = ws > 1 or args.ddp
+    if use_dist:
         import torch.distributed as dist
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
         dist.init_process_group("nccl", device_id=dev)
 
     torch.backends.cudnn.benchmark = False          # autotuning would probe workspaces past the budget
@@ -207,7 +212,7 @@ def main():
         model = getattr(torchvision.models, args.arch)().to(dev)
         shape_desc = f"{args.arch} {size}^2 fp32"
     base_model = model
-    if ws > 1:
+    if use_dist:
         model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
     loss_fn = torch.nn.functional.cross_entropy
@@ -246,6 +251,20 @@ def main():
         ctx.synchronize()
         return ok
 
+    lms = None
+
+    def rewrap():
+        """A step that failed inside DDP's backward leaves its reducer mid-iteration;
+        a fresh wrapper (collective: every rank calls this together) resets it."""
+        nonlocal model
+        if not use_dist:
+            return
+        model = None
+        gc.collect()
+        model = torch.nn.parallel.DistributedDataParallel(base_model, device_ids=[local])
+        if lms is not None:
+            lms.model = model
+
     def agree(v, op="min"):
         if ws == 1:
             return v
@@ -265,6 +284,7 @@ def main():
             ctx.reset_peaks()
             ok = agree(1.0 if fits(hi) else 0.0) > 0.5
             if not ok:
+                rewrap()
                 break
             peaks[hi] = ctx.stats()["device_peak"]
             lo, hi = hi, hi * 2
@@ -274,6 +294,8 @@ def main():
             mid = (lo + hi) // 2
             ctx.reset_peaks()
             ok = agree(1.0 if fits(mid) else 0.0) > 0.5
+            if not ok:
+                rewrap()
             if ok:
                 peaks[mid] = ctx.stats()["device_peak"]
                 lo = mid
@@ -370,6 +392,7 @@ def main():
         attempts.append({"batch": nb, "n_tensors": n_tensors, "ok": ok})
         ok = agree(1.0 if ok else 0.0) > 0.5
         if not ok:
+            rewrap()
             opt.zero_grad(set_to_none=True)
             gc.collect()
             torch.cuda.synchronize(dev)
@@ -444,6 +467,7 @@ def main():
                 raise
             log(f"[bench] timed run OOM with n_tensors={n_use}; trying more tensors")
             traceback.clear_frames(e.__traceback__)
+            rewrap()
             opt.zero_grad(set_to_none=True)
             gc.collect()
             torch.cuda.synchronize(dev)
@@ -545,7 +569,7 @@ def main():
                    "model": args.arch, "global_batch": bs * ws, "per_gpu_batch": bs,
                    "budget_gib": budget / GIB, "no_swap_max_batch": b0,
                    "batch_ratio": round(bs / b0, 3) if b0 else None, "input_size": size,
-                   "parallelism": f"dp{ws}" if ws > 1 else "single",
+                   "parallelism": f"dp{ws}" if use_dist else "single",
                    "l2": "inputs (>=450 MB/step) exceed L2; no flush",
                    "rewrite": {"lb": args.lb, "ub": args.ub, "ctrld_strategy": args.strategy,
                                "fuse_swapins": args.fuse_swapins, "n_tensors": plan.report.tensors_swapped},
@@ -583,7 +607,7 @@ def main():
                 json.dump({"items": ctx.plan_items(), "plan_info": ctx.plan_info()}, fh)
         except OSError:
             pass
-    if ws > 1:
+    if use_dist:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
