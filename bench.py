@@ -535,7 +535,11 @@ def main():
         p["wire_gbs"] = round(p["bytes"] / max(p["ms"], 1e-9) / 1e6, 2)
         p["logical_gbs"] = round(p["logical"] / max(p["ms"], 1e-9) / 1e6, 2)
         p["ms"] = round(p["ms"], 1)
-    dom_key = max(paths, key=lambda k: paths[k]["ms"]) if paths else None
+    # the roofline names our dominant kernel path (ZVC / SM zero-copy); copy-engine
+    # transfers (no kernel of ours) are reported in transfer_paths alongside
+    kernel_paths = [k for k in paths if not k.endswith("copy-engine")]
+    dom_key = (max(kernel_paths, key=lambda k: paths[k]["ms"]) if kernel_paths
+               else max(paths, key=lambda k: paths[k]["ms"]) if paths else None)
     link_peak = max(link.get("d2h", 0), link.get("h2d", 0)) if link else None
     if dom_key:
         dom_peak = link.get(dom_key.split(":")[0]) if link else None
