@@ -307,6 +307,15 @@ class Context:
         return w.value
 
     # -- pools --------------------------------------------------------------------
+    def dev_alloc(self, nbytes: int, stream=None) -> int:
+        """Raw device block from this context's pool (for tests / non-torch callers)."""
+        p = ctypes.c_void_p()
+        _check(lib().lms_dev_alloc(self.ptr, nbytes, _stream_ptr(stream), ctypes.byref(p)), "lms_dev_alloc")
+        return p.value
+
+    def dev_free(self, ptr: int, stream=None):
+        _check(lib().lms_dev_free(self.ptr, ptr, _stream_ptr(stream)), "lms_dev_free")
+
     def hold_until(self, t, stream=None):
         _check(lib().lms_dev_hold_until(self.ptr, t.data_ptr(), _stream_ptr(stream)), "lms_dev_hold_until")
 
@@ -371,6 +380,19 @@ def plan_solve(sizes, t_alloc, t_free):
     _check(lib().lms_plan_solve(u64(*sizes), _i64(list(t_alloc)), _i64(list(t_free)), n, offs,
                                 ctypes.byref(region)), "lms_plan_solve")
     return [None if offs[i] == 2 ** 64 - 1 else offs[i] for i in range(n)], region.value
+
+
+class DeviceBuffer:
+    """A raw pool block seen as a CUDA array (``__cuda_array_interface__``), so
+    ``torch.as_tensor(buf, device="cuda")`` views it without a copy."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = ptr, nbytes
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False), "version": 3,
+                "stream": None}
 
 
 _installed: Context | None = None

@@ -1,0 +1,79 @@
+"""Device pool under fragmentation: page moves must never corrupt live data.
+
+A second context with its own small budget (not the allocator of the test
+session) is fragmented until an allocation that fits the budget only by
+moving physical pages; every live block keeps its contents, the moved-to
+block is fully writable, and trimming the stale aliases keeps it so.  This is
+the pool's version of the reference's residency model (sim.py:116-124,
+:193-211): bytes stay with their owner until it frees them.
+"""
+
+import pytest
+import torch
+
+from paper_1807_02037_b200 import runtime as rt
+
+pytestmark = pytest.mark.gpu
+
+MIB = 1 << 20
+
+
+def _view(ptr, nbytes):
+    return torch.as_tensor(rt.DeviceBuffer(ptr, nbytes), device="cuda")
+
+
+def test_page_moves_keep_live_blocks_intact(lms_ctx):
+    ctx = rt.Context(device=0, device_reserve=1 << 30, timing=False)   # 16 pages of 64 MiB
+    try:
+        blocks = []
+        for i in range(12):   # 12 one-page blocks, then 4 free pages at the end
+            p = ctx.dev_alloc(64 * MIB)
+            v = _view(p, 64 * MIB)
+            v.fill_(i + 1)
+            blocks.append((p, i + 1))
+        torch.cuda.synchronize()
+        # free every other block: plenty of free bytes, no contiguous run big enough
+        for p, _ in blocks[1:11:2]:   # 1,3,5,7,9: one-page holes; 11 stays, so the free tail is 4 pages
+            ctx.dev_free(p)
+        keep = blocks[0::2] + [blocks[11]]
+        torch.cuda.synchronize()
+        before = ctx.stats()
+        big = ctx.dev_alloc(320 * MIB)     # 5 pages: fits only with pages moved (aliased) under fresh VA
+        after = ctx.stats()
+        vb = _view(big, 320 * MIB)
+        vb.fill_(0xAB)
+        torch.cuda.synchronize()
+        for p, val in keep:
+            assert bool((_view(p, 64 * MIB) == val).all()), "a live block changed after a page move"
+        assert bool((vb == 0xAB).all())
+        assert after["n_reclaims"] > before["n_reclaims"]
+        # trimming the stale VA aliases must not touch live data either
+        torch.cuda.synchronize()
+        ctx.trim()
+        for p, val in keep:
+            assert bool((_view(p, 64 * MIB) == val).all())
+        assert bool((vb == 0xAB).all())
+        ctx.dev_free(big)
+        for p, _ in keep:
+            ctx.dev_free(p)
+        # the whole budget is usable again after the moves
+        p = ctx.dev_alloc(900 * MIB)
+        _view(p, 900 * MIB).fill_(7)
+        torch.cuda.synchronize()
+        ctx.dev_free(p)
+    finally:
+        torch.cuda.synchronize()
+        ctx.close()
+
+
+def test_budget_is_physical(lms_ctx):
+    ctx = rt.Context(device=0, device_reserve=256 * MIB, timing=False)
+    try:
+        p = ctx.dev_alloc(200 * MIB)
+        with pytest.raises(rt.LmsOutOfMemoryError):
+            ctx.dev_alloc(100 * MIB)
+        ctx.dev_free(p)
+        q = ctx.dev_alloc(250 * MIB)
+        ctx.dev_free(q)
+    finally:
+        ctx.close()
