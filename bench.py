@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--strategy", default="chain_rule")
     ap.add_argument("--fuse-swapins", action="store_true", default=True)
     ap.add_argument("--no-fuse-swapins", dest="fuse_swapins", action="store_false")
+    ap.add_argument("--fuse-distance", type=int, default=1, help="RewriteConfig.swapin_fuse_distance")
     ap.add_argument("--b0", type=int, default=0, help="skip bisection and use this no-swap batch")
     ap.add_argument("--n-tensors", type=int, default=0,
                     help="swap only the first n candidate tensors (rewrite BFS order); -1 = all; "
@@ -62,6 +63,8 @@ def parse():
                     help="probes of the n_tensors bisection (0: swap every candidate tensor)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--tf32", action="store_true")
+    ap.add_argument("--same-batch", type=int, default=1,
+                    help="also time TFLMS (every candidate swapped) at B0 against the plain step at B0")
     ap.add_argument("--ddp", action="store_true",
                     help="wrap the model in DistributedDataParallel even at one rank (exercises the DP path)")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
@@ -343,7 +346,7 @@ def main():
     else:
         xc, yc = batch(cap_b)
     cfg0 = RewriteConfig(lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
-                         fuse_swapins=args.fuse_swapins, swapin_fuse_distance=1)
+                         fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance)
     codec = args.codec
     # tensors under 64 KiB at the capture size stay on the device
     lms = LMS(model, loss_fn, opt, cfg0, ctx, codec=codec, min_swap_bytes=64 << 10)
@@ -373,7 +376,7 @@ def main():
     def try_swap(nb, n_tensors):
         """Run ``warmup`` swapped steps at batch nb; True if they fit the budget."""
         cfg = RewriteConfig(n_tensors=n_tensors, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
-                            fuse_swapins=args.fuse_swapins, swapin_fuse_distance=1)
+                            fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance)
         lms.replan(cfg)
         lms.static_plan = False   # fit probes run on the dynamic pool; the timed run plans
         xb, yb = batch(nb, seed=7)
@@ -449,7 +452,7 @@ def main():
     for n_use in sorted(set(ok_ns)):
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
                                  ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
-                                 swapin_fuse_distance=1))
+                                 swapin_fuse_distance=args.fuse_distance))
         try:
             for _ in range(args.warmup):
                 lms.step(xs, ys)
@@ -497,6 +500,21 @@ def main():
     e2e_step()
     e2e_ms = timed(torch, dev, ws, e2e_step, args.steps, tag="e2e")
     e2e_val = bs * ws * args.steps / (e2e_ms * 1e-3)
+
+    # ---- 5b. overhead at the same batch: TFLMS on (every candidate swapped) vs off at B0
+    same_batch = None
+    if b0 > 0 and args.same_batch:
+        x0, y0 = batch(b0, seed=3)
+        lms.replan(RewriteConfig(n_tensors=-1, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
+                                 fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance))
+        for _ in range(max(3, args.warmup)):
+            lms.step(x0, y0)
+        sb_ms = timed(torch, dev, ws, lambda: lms.step(x0, y0), args.steps, tag="swapped_at_b0")
+        same_batch = {"batch": b0, "swapped_ms_per_step": round(sb_ms / args.steps, 3),
+                      "no_swap_ms_per_step": round(noswap_ms / args.steps, 3),
+                      "overhead": round(sb_ms / noswap_ms - 1.0, 4)}
+        x0 = y0 = None
+        gc.collect()
 
     # ---- 6. link peak, CPU baseline -----------------------------------------
     if rank != 0:
@@ -581,7 +599,8 @@ def main():
         "no_swap": {"batch": b0, "img_s": round(noswap_ips, 2) if noswap_ips else None,
                     "ms_per_step": round(noswap_ms / steps, 3) if noswap_ms else None},
         "overhead": {"paper_framing": round(noswap_ips / value - 1.0, 4) if noswap_ips else None,
-                     "note": "img/s at B0 without swap / img/s at 4.7xB0 with swap - 1"},
+                     "note": "img/s at B0 without swap / img/s at 4.7xB0 with swap - 1",
+                     "same_batch": same_batch},
         "swap": {"tensors_swapped": plan.report.tensors_swapped, "swap_ins": len(plan.groups),
                  "control_edges": plan.report.control_edges_added,
                  "d2h_bytes_per_step": d2h_b // steps, "h2d_bytes_per_step": h2d_b // steps,

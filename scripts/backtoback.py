@@ -20,10 +20,15 @@ def main():
     ap.add_argument("--batch", type=int, default=908)
     ap.add_argument("--budget-gib", type=float, default=16.0)
     ap.add_argument("--codec", default="auto")
+    ap.add_argument("--tf32", action="store_true")
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--e2e", action="store_true")
     ap.add_argument("--no-plan", action="store_true")
     ap.add_argument("--no-trim", action="store_true")
+    ap.add_argument("--refine", default="2", help="comma list of steps that refine the plan")
+    ap.add_argument("--n-tensors", type=int, default=-1)
+    ap.add_argument("--pre", default="", help="comma list of n_tensors: 2 dynamic steps each before the run "
+                                            "(what bench.py's fit probes do)")
     args = ap.parse_args()
 
     import torch
@@ -34,6 +39,9 @@ def main():
     ctx = rt.Context(device=0, device_reserve=int(args.budget_gib * (1 << 30)), host_chunk=4 << 30, timing=True)
     rt.install_allocator(ctx)
     torch.backends.cudnn.benchmark = False
+    # strict fp32 like bench.py (the BASELINE config); --tf32 lets cuDNN use TF32 tensor cores
+    torch.backends.cudnn.allow_tf32 = bool(args.tf32)
+    torch.backends.cuda.matmul.allow_tf32 = bool(args.tf32)
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     model = torchvision.models.resnet50().to(dev)
@@ -41,20 +49,29 @@ def main():
     lf = torch.nn.functional.cross_entropy
     lms = LMS(model, lf, opt, RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1), ctx, codec=args.codec,
               min_swap_bytes=64 << 10, static_plan=not args.no_plan)
+    LMS.REFINE_STEPS = tuple(int(x) for x in args.refine.split(",") if x)
     if args.no_trim:
         ctx.trim = lambda: 0
     xc = torch.randn(4, 3, 224, 224, device=dev)
     yc = torch.randint(0, 1000, (4,), device=dev)
     lms.capture(xc, yc)
-    del xc, yc
     x = torch.randn(args.batch, 3, 224, 224, device=dev)
     y = torch.randint(0, 1000, (args.batch,), device=dev)
+    for n_pre in [int(v) for v in args.pre.split(",") if v]:
+        lms.replan(RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1, n_tensors=n_pre))
+        lms.static_plan = False
+        for _ in range(2):
+            lms.step(x, y)
+        torch.cuda.synchronize()
+    lms.static_plan = not args.no_plan
+    lms.replan(RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1, n_tensors=args.n_tensors))
+    del xc, yc
     if args.e2e:
         xh, yh = x.cpu().pin_memory(), y.cpu().pin_memory()
         del x, y
     s = torch.cuda.current_stream()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    keys = ("n_reclaims", "pool_driver_ms", "unmap_ms", "map_ms", "access_ms", "alloc_wait_ms", "n_device_syncs")
+    keys = ("n_reclaims", "pool_driver_ms", "alloc_wait_ms", "n_device_syncs")
     host = []
     torch.cuda.synchronize()
     evs[0].record(s)

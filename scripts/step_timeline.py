@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--batch", type=int, default=908)
     ap.add_argument("--budget-gib", type=float, default=16.0)
     ap.add_argument("--codec", default="auto")
+    ap.add_argument("--tf32", action="store_true")
     ap.add_argument("--lb", type=int, default=1)
     ap.add_argument("--ub", type=int, default=10000)
     ap.add_argument("--strategy", default="chain_rule")
@@ -64,6 +65,9 @@ def main():
     ctx = rt.Context(device=0, device_reserve=int(args.budget_gib * (1 << 30)), host_chunk=4 << 30, timing=True)
     rt.install_allocator(ctx)
     torch.backends.cudnn.benchmark = False
+    # strict fp32 like bench.py (the BASELINE config); --tf32 lets cuDNN use TF32 tensor cores
+    torch.backends.cudnn.allow_tf32 = bool(args.tf32)
+    torch.backends.cuda.matmul.allow_tf32 = bool(args.tf32)
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     model = torchvision.models.resnet50().to(dev)
