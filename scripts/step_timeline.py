@@ -143,6 +143,21 @@ def main():
         "device_peak_GB": st["device_peak"] / 1e9, "plan_info": ctx.plan_info(),
     }
     print(json.dumps(res, indent=1))
+    # Chrome trace (chrome://tracing / Perfetto) of the last step: compute windows and
+    # every transfer on its copy channel, from CUDA events (no nsys in this image)
+    ev = [{"name": "forward", "ph": "X", "pid": 0, "tid": 0, "ts": 0.0, "dur": (tf - t0) * 1e3},
+          {"name": "backward+optimizer", "ph": "X", "pid": 0, "tid": 0, "ts": (tf - t0) * 1e3,
+           "dur": (te - tf) * 1e3}]
+    names = {0: "copy-engine", 1: "sm-zero-copy", 2: "zvc"}
+    for r in tr:
+        ev.append({"name": f"{'swap-out' if r['direction'] == 0 else 'swap-in'} {names.get(r['codec'])} "
+                           f"{r['logical_bytes'] / 2**20:.0f} MiB -> {r['wire_bytes'] / 2**20:.0f} MiB",
+                   "ph": "X", "pid": 0, "tid": 1 + r["direction"], "ts": (r["start_ms"] - t0) * 1e3,
+                   "dur": (r["end_ms"] - r["start_ms"]) * 1e3})
+    meta = [{"name": "thread_name", "ph": "M", "pid": 0, "tid": k, "args": {"name": n}}
+            for k, n in ((0, "compute stream"), (1, "D2H channel"), (2, "H2D channel"))]
+    with open(os.path.join(ROOT, "gpurun_out", f"timeline_{args.codec}_{args.batch}.json"), "w") as fh:
+        json.dump({"traceEvents": meta + ev, "displayTimeUnit": "ms"}, fh)
     items = ctx.plan_items()
     if items:
         with open(os.path.join(ROOT, "gpurun_out", f"plan_items_{args.codec}_{args.batch}.json"), "w") as fh:
