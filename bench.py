@@ -167,8 +167,19 @@ def measure_host_link(torch, dev, nbytes=512 * MIB):
 def is_oom(exc) -> bool:
     """Budget exhaustion, including cuDNN's report of a workspace it could not allocate."""
     msg = str(exc)
-    return ("LMS_OOM" in msg or "out of memory" in msg.lower()
+    return ("LMS_OOM" in msg or "out of memory" in msg.lower() or "pinned host limit" in msg
             or "unable to find an engine" in msg or "CUDNN_STATUS_ALLOC_FAILED" in msg)
+
+
+def host_available() -> int:
+    """MemAvailable of this host (bytes)."""
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 64 << 30
 
 
 def main():
@@ -188,7 +199,11 @@ def main():
     budget = int(args.budget_gib * GIB) if not args.quick else 4 * GIB
 
     # the pool must own PyTorch's allocator before anything lazily initialises CUDA
-    ctx = rt.Context(device=local, device_reserve=budget, host_chunk=4 * GIB, timing=True)
+    # pinned host memory is shared by the ranks of this box: each gets its share
+    # (80 % of MemAvailable / local ranks), enforced by the host pool
+    local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", ws))
+    host_cap = int(0.8 * host_available() / max(1, local_ws))
+    ctx = rt.Context(device=local, device_reserve=budget, host_chunk=4 * GIB, timing=True, host_limit=host_cap)
     rt.install_allocator(ctx)
     torch.cuda.set_device(local)
     # the link's copy-engine peak, measured first while the pool is empty
@@ -367,6 +382,15 @@ def main():
     while n_t < len(order) and acc * bs < 1.15 * need:
         acc += order[n_t]
         n_t += 1
+    # the host must hold every swapped tensor of the step (ZVC reserves its bound)
+    host_per_img = 1.1 * sum(order)
+    host_limited = False
+    if host_per_img * bs > host_cap:
+        bs_host = int(host_cap / host_per_img)
+        log(f"[bench] host memory caps the swapped batch: {host_cap / GIB:.0f} GiB pinned per rank "
+            f"-> batch {bs_host} (target {bs})")
+        bs = max(b0, min(bs, bs_host))
+        host_limited = True
     log(f"[bench] swap batch {bs}: {len(order)} candidate tensors, {sum(order) / MIB:.1f} MiB/img; "
         f"need {need / GIB:.2f} GiB off-device -> n_tensors={n_t}")
 
@@ -591,6 +615,7 @@ def main():
                    "model": args.arch, "global_batch": bs * ws, "per_gpu_batch": bs,
                    "budget_gib": budget / GIB, "no_swap_max_batch": b0,
                    "batch_ratio": round(bs / b0, 3) if b0 else None, "input_size": size,
+                   "host_limit_gib_per_rank": round(host_cap / GIB, 1), "host_limited": host_limited,
                    "parallelism": f"dp{ws}" if use_dist else "single",
                    "l2": "inputs (>=450 MB/step) exceed L2; no flush",
                    "rewrite": {"lb": args.lb, "ub": args.ub, "ctrld_strategy": args.strategy,

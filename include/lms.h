@@ -68,6 +68,8 @@ typedef struct {
   int overlap_transfers;      /* 1: separate D2H/H2D streams (sim.py:287-290) */
   int timing;                 /* 1: record per-transfer timing events */
   int sm_ctas;                /* CTAs for SM-driven transfer/codec kernels (0 = auto) */
+  size_t host_limit;          /* cap on pinned host bytes (0 = none); swap-outs past it fail
+                                 with LMS_E_HOST_OOM instead of pinning the host into swap */
 } lms_config_t;
 
 typedef struct {

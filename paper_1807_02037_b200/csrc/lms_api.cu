@@ -605,6 +605,12 @@ int host_alloc_locked(lms_ctx* c, size_t size, void** out) {
     }
   }
   size_t grow = std::max(need, c->cfg.host_chunk ? c->cfg.host_chunk : (size_t(1) << 30));
+  if (c->cfg.host_limit) {
+    if (c->host_reserved + need > c->cfg.host_limit)
+      return fail(LMS_E_HOST_OOM, "pinned host limit reached (" + std::to_string(c->host_reserved) + " of " +
+                                      std::to_string(c->cfg.host_limit) + " bytes pinned)");
+    grow = std::min(grow, c->cfg.host_limit - c->host_reserved);
+  }
   void* p = nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaHostAlloc(&p, grow, cudaHostAllocPortable | cudaHostAllocMapped);

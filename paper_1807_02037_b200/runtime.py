@@ -35,7 +35,7 @@ class _Config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("device_reserve", ctypes.c_size_t),
                 ("device_limit", ctypes.c_size_t), ("host_reserve", ctypes.c_size_t),
                 ("host_chunk", ctypes.c_size_t), ("overlap_transfers", ctypes.c_int),
-                ("timing", ctypes.c_int), ("sm_ctas", ctypes.c_int)]
+                ("timing", ctypes.c_int), ("sm_ctas", ctypes.c_int), ("host_limit", ctypes.c_size_t)]
 
 
 _STAT_FIELDS = [
@@ -134,7 +134,7 @@ def _check(rc: int, what: str):
     msg = f"{what}: {lib().lms_last_error().decode()}"
     if rc == LMS_E_INVALID:
         raise ValueError(msg)
-    if rc == LMS_E_OOM:
+    if rc in (LMS_E_OOM, LMS_E_HOST_OOM):
         raise LmsOutOfMemoryError(msg)
     raise LmsError(msg)
 
@@ -170,13 +170,14 @@ class Context:
 
     def __init__(self, device: int = 0, device_reserve: int = 0, device_limit: int = 0,
                  host_reserve: int = 0, host_chunk: int = 1 << 30, overlap_transfers: bool = True,
-                 timing: bool = False, sm_ctas: int = 0):
+                 timing: bool = False, sm_ctas: int = 0, host_limit: int = 0):
         L = lib()
         cfg = _Config()
         _check(L.lms_default_config(ctypes.byref(cfg)), "lms_default_config")
         cfg.device, cfg.device_reserve, cfg.device_limit = device, device_reserve, device_limit
         cfg.host_reserve, cfg.host_chunk = host_reserve, host_chunk
         cfg.overlap_transfers, cfg.timing, cfg.sm_ctas = int(overlap_transfers), int(timing), sm_ctas
+        cfg.host_limit = host_limit
         out = ctypes.c_void_p()
         _check(L.lms_create(ctypes.byref(cfg), ctypes.byref(out)), "lms_create")
         self.ptr = out.value
