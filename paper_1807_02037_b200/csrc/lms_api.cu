@@ -1351,6 +1351,30 @@ int lms_host_alloc(lms_ctx* c, size_t size, void** out) {
   return host_alloc_locked(c, size, out);
 }
 
+int lms_host_reserve(lms_ctx* c, size_t total) {
+  if (!c) return fail(LMS_E_INVALID, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  if (c->cfg.host_limit) total = std::min(total, c->cfg.host_limit);
+  const size_t chunk = c->cfg.host_chunk ? c->cfg.host_chunk : (size_t(1) << 30);
+  while (c->host_reserved < total) {
+    const size_t grow = std::min(chunk, total - c->host_reserved);
+    void* q = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaHostAlloc(&q, grow, cudaHostAllocPortable | cudaHostAllocMapped);
+    c->st.host_grow_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LMS_E_HOST_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    }
+    c->st.n_host_grow++;
+    auto* a = new Arena();
+    a->init(static_cast<char*>(q), grow);
+    c->chunks.push_back({static_cast<char*>(q), a});
+    c->host_reserved += grow;
+  }
+  return LMS_OK;
+}
+
 int lms_host_free(lms_ctx* c, void* ptr) {
   if (!c) return fail(LMS_E_INVALID, "null ctx");
   std::lock_guard<std::mutex> g(c->mu);

@@ -103,6 +103,7 @@ def lib():
         "lms_dev_alloc": ([vp, sz, vp, pp], i), "lms_dev_free": ([vp, vp, vp], i),
         "lms_dev_hold_until": ([vp, vp, vp], i),
         "lms_host_alloc": ([vp, sz, pp], i), "lms_host_free": ([vp, vp], i),
+        "lms_host_reserve": ([vp, sz], i),
         "lms_swap_out": ([vp, vp, i64p, i64p, i, i, vp, i, pp], i),
         "lms_swap_in": ([vp, vp, vp, i64p, vp], i), "lms_swap_wait": ([vp, vp, vp], i),
         "lms_swap_out_done": ([vp, vp], i), "lms_handle_release": ([vp, vp], i),
@@ -316,6 +317,10 @@ class Context:
 
     def dev_free(self, ptr: int, stream=None):
         _check(lib().lms_dev_free(self.ptr, ptr, _stream_ptr(stream)), "lms_dev_free")
+
+    def host_reserve(self, total: int):
+        """Grow the pinned pool to ``total`` reserved bytes now (outside timed steps)."""
+        _check(lib().lms_host_reserve(self.ptr, total), "lms_host_reserve")
 
     def hold_until(self, t, stream=None):
         _check(lib().lms_dev_hold_until(self.ptr, t.data_ptr(), _stream_ptr(stream)), "lms_dev_hold_until")
