@@ -481,7 +481,8 @@ def main():
             while n_host > 0 and not try_swap(bs, n_host if n_host < N else -1):
                 n_host //= 2
             ok_ns = [n_host] if n_host < N else [N]
-        ok_ns = [N]
+        else:
+            ok_ns = [N]
     xs, ys = batch(bs, seed=7)
 
     # timed run with the fewest tensors that fitted; a run that hits the budget
