@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--size", type=int, default=0, help="input edge (224 for classifiers, 192 for unet3d)")
     ap.add_argument("--budget-gib", type=float, default=16.0)
     ap.add_argument("--factor", type=float, default=4.7)
+    ap.add_argument("--batch", type=int, default=0, help="swapped batch (default: factor x B0)")
     ap.add_argument("--codec", default="auto", choices=["ce", "sm", "zvc", "auto"])
     ap.add_argument("--lb", type=int, default=1)
     ap.add_argument("--ub", type=int, default=10000)
@@ -350,7 +351,7 @@ def main():
         log(f"[bench] no-swap B0={b0}: {noswap_ips:.1f} img/s ({noswap_ms / args.steps:.1f} ms/step)")
 
     # ---- 3. capture + rewrite, choose how many tensors to swap ----------------
-    bs = max(1, int(math.ceil(args.factor * b0)))
+    bs = args.batch or max(1, int(math.ceil(args.factor * b0)))
     # capture: one traced step of the same model at a small batch (the graph
     # does not depend on batch or spatial size; tensor bytes scale with both)
     cap_b = 4
