@@ -701,4 +701,87 @@ __global__ void __launch_bounds__(32) tma_copy_kernel(const __grid_constant__ CU
   bulk_wait<0>();
 }
 
+// -------------------------------------------------------------------------
+// TMA transpose pack/unpack: the strided side's unit-stride dim is not its
+// innermost one (e.g. a channels-last view of an NCHW tensor).  Tiles of
+// T x T elements (T * E = 128 B) are loaded by cp.async.bulk.tensor with the
+// 128 B swizzle, transposed through shared memory by the CTA (the swizzle
+// keeps the row-side accesses conflict-free), and stored by
+// cp.async.bulk.tensor with the same swizzle from a second buffer.  One
+// elected thread drives the TMA engine; loads run STAGES tiles ahead.
+
+__device__ __forceinline__ uint32_t swz128(uint32_t row, uint32_t byte_col) {
+  return row * 128u + ((((byte_col >> 4) ^ (row & 7u))) << 4) + (byte_col & 15u);
+}
+
+// Each warp runs its own two-deep pipeline (no CTA-wide barriers: lane 0
+// drives the TMA engine, the warp transposes): the block-synchronous first
+// version spent two thirds of its cycles waiting at __syncthreads.
+template <int E, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) tma_transpose_kernel(const __grid_constant__ CUtensorMap src,
+                                                                   const __grid_constant__ CUtensorMap dst,
+                                                                   TmaBoxGrid g) {
+  using W = typename Word<E>::T;
+  constexpr uint32_t T = 128 / E;
+  constexpr uint32_t kTile = T * 128;  // bytes
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  __shared__ __align__(8) uint64_t bar[WARPS][2];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm) + 1023) & ~uintptr_t(1023));
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* in = base + warp * 4 * kTile;   // 2 input tiles, then 2 output tiles
+  unsigned char* out = in + 2 * kTile;
+  auto coords = [&](uint64_t b, int c[5]) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t q = uint32_t(b % g.nbox[k]);
+      b /= g.nbox[k];
+      c[k] = int(q * g.box[k]);
+    }
+  };
+  const uint64_t nw = uint64_t(gridDim.x) * WARPS;
+  uint64_t t = uint64_t(blockIdx.x) * WARPS + warp;
+  int c[5];
+  if (lane == 0) {
+    mbar_init(&bar[warp][0], 1);
+    mbar_init(&bar[warp][1], 1);
+    fence_mbar_init();
+    if (t < g.total) {
+      coords(t, c);
+      mbar_expect_tx(&bar[warp][0], kTile);
+      tma_load_5d(in, &src, c, &bar[warp][0]);
+    }
+  }
+  __syncwarp();
+  uint32_t phases = 0;
+  for (uint32_t k = 0; t < g.total; t += nw, ++k) {
+    const uint32_t b = k & 1u;
+    if (lane == 0 && t + nw < g.total) {  // prefetch the next tile into the other buffer
+      coords(t + nw, c);
+      mbar_expect_tx(&bar[warp][b ^ 1u], kTile);
+      tma_load_5d(in + (b ^ 1u) * kTile, &src, c, &bar[warp][b ^ 1u]);
+    }
+    mbar_wait(&bar[warp][b], (phases >> b) & 1u);
+    phases ^= 1u << b;
+    if (lane == 0) bulk_wait_read<1>();  // the store that last read out[b] is done reading
+    __syncwarp();
+    const unsigned char* A = in + b * kTile;
+    unsigned char* B = out + b * kTile;
+    // B[r][col] = A[col][r]: lane = col walks a B row (conflict-free stores)
+#pragma unroll 8
+    for (uint32_t r = 0; r < T; ++r)
+      for (uint32_t col = lane; col < T; col += 32)
+        *reinterpret_cast<W*>(B + swz128(r, col * E)) = *reinterpret_cast<const W*>(A + swz128(col, r * E));
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      coords(t, c);
+      int sc[5] = {c[1], c[0], c[2], c[3], c[4]};
+      tma_store_5d(&dst, sc, B);
+      bulk_commit();
+    }
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
 }  // namespace lms

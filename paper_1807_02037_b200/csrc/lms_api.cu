@@ -825,6 +825,110 @@ int launch_tma_rows(lms_ctx* c, char* dst, const char* src, int nd, const int64_
   return 0;
 }
 
+// warps per CTA of the TMA transpose (each holds 4 tiles of (128/E) x 128 B)
+template <int E>
+constexpr int tt_warps() { return E == 1 ? 2 : 4; }
+constexpr int kTmaTWarps = 4;
+
+template <int E>
+size_t tma_transpose_smem() { return 1024 + size_t(tt_warps<E>()) * 4 * (128 / E) * 128; }
+
+// Transposed layouts (the strided side's unit-stride dim `cd` is not its last
+// dim) through 128 B-swizzled tensor maps.  Same contract as launch_tma_rows.
+template <bool PACK>
+int launch_tma_transpose(lms_ctx* c, char* dst, const char* src, int nd, const int64_t* sizes,
+                         const int64_t* strides, int elem, cudaStream_t s) {
+  if (!c->use_tma_pack || nd < 2) return 1;
+  if (reinterpret_cast<uintptr_t>(dst) % 16 || reinterpret_cast<uintptr_t>(src) % 16) return 1;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return 1;
+  const int last = nd - 1;
+  int cd = -1;
+  for (int k = 0; k < last; ++k)
+    if (strides[k] == 1) cd = k;
+  if (cd < 0 || strides[last] == 1) return 1;
+  // contiguous-side (row-major) strides
+  int64_t cst[LMS_MAX_DIMS + 1];
+  {
+    int64_t acc = 1;
+    for (int k = nd - 1; k >= 0; --k) {
+      cst[k] = acc;
+      acc *= sizes[k];
+    }
+  }
+  // batch dims (all but cd and last), innermost first, merged where both sides allow
+  int64_t bz[LMS_MAX_DIMS], bs_s[LMS_MAX_DIMS], bs_c[LMS_MAX_DIMS];
+  int nb = 0;
+  for (int k = last - 1; k >= 0; --k) {
+    if (k == cd) continue;
+    if (nb > 0 && bs_s[nb - 1] * bz[nb - 1] == strides[k] && bs_c[nb - 1] * bz[nb - 1] == cst[k]) {
+      bz[nb - 1] *= sizes[k];
+      continue;
+    }
+    bz[nb] = sizes[k];
+    bs_s[nb] = strides[k];
+    bs_c[nb] = cst[k];
+    ++nb;
+  }
+  if (nb > 3) return 1;
+  const uint32_t T = 128 / elem;
+  // strided map: d0 = cd (unit), d1 = last; contiguous map: d0 = last (unit), d1 = cd
+  cuuint64_t gs[5], gc[5], ss[4], sc[4];
+  gs[0] = sizes[cd];
+  gs[1] = sizes[last];
+  ss[0] = uint64_t(strides[last]) * elem;
+  gc[0] = sizes[last];
+  gc[1] = sizes[cd];
+  sc[0] = uint64_t(cst[cd]) * elem;
+  for (int i = 0; i < 3; ++i) {
+    const bool real = i < nb;
+    gs[2 + i] = gc[2 + i] = real ? cuuint64_t(bz[i]) : 1;
+    ss[1 + i] = real ? uint64_t(bs_s[i]) * elem : ss[i] * gs[1 + i];
+    sc[1 + i] = real ? uint64_t(bs_c[i]) * elem : sc[i] * gc[1 + i];
+  }
+  for (int i = 0; i < 4; ++i)
+    if (ss[i] % 16 || sc[i] % 16 || ss[i] >= (uint64_t(1) << 40) || sc[i] >= (uint64_t(1) << 40)) return 1;
+  for (int i = 0; i < 5; ++i)
+    if (gs[i] > (uint64_t(1) << 32)) return 1;
+  CUtensorMapDataType dt = elem == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                           : elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                           : elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                       : CU_TENSOR_MAP_DATA_TYPE_UINT64;
+  cuuint32_t box[5] = {T, T, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+  const char* strided = PACK ? src : dst;
+  const char* contig = PACK ? dst : src;
+  CUtensorMap m_s, m_c;
+  if (enc(&m_s, dt, 5, const_cast<char*>(strided), gs, ss, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS ||
+      enc(&m_c, dt, 5, const_cast<char*>(contig), gc, sc, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+    return 1;
+  // the box grid walks the LOAD map's dims
+  const cuuint64_t* gl = PACK ? gs : gc;
+  TmaBoxGrid g{};
+  g.total = 1;
+  for (int i = 0; i < 5; ++i) {
+    g.box[i] = box[i];
+    g.nbox[i] = uint32_t((gl[i] + box[i] - 1) / box[i]);
+    g.total *= g.nbox[i];
+  }
+  const CUtensorMap& ld = PACK ? m_s : m_c;
+  const CUtensorMap& st = PACK ? m_c : m_s;
+  static const int per_sm = getenv("LMS_TMA_T_CTAS") ? std::max(1, atoi(getenv("LMS_TMA_T_CTAS"))) : 12;
+  const int grid = int(std::min<uint64_t>((g.total + kTmaTWarps - 1) / kTmaTWarps, uint64_t(c->num_sms) * per_sm));
+  switch (elem) {
+    case 1: tma_transpose_kernel<1, tt_warps<1>()><<<grid, 32 * tt_warps<1>(), tma_transpose_smem<1>(), s>>>(ld, st, g); break;
+    case 2: tma_transpose_kernel<2, tt_warps<2>()><<<grid, 32 * tt_warps<2>(), tma_transpose_smem<2>(), s>>>(ld, st, g); break;
+    case 4: tma_transpose_kernel<4, tt_warps<4>()><<<grid, 32 * tt_warps<4>(), tma_transpose_smem<4>(), s>>>(ld, st, g); break;
+    default: tma_transpose_kernel<8, tt_warps<8>()><<<grid, 32 * tt_warps<8>(), tma_transpose_smem<8>(), s>>>(ld, st, g); break;
+  }
+  c->st.kernel_launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
 // pack (dst contiguous) or unpack (dst strided); either side may be mapped host memory
 template <bool PACK>
 int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_t* sizes_in,
@@ -865,8 +969,9 @@ int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_
     default: KERNEL<PACK, 8><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                 \
   }
   const int last = nd - 1;
-  if (strides[last] == 1 && !is_host_ptr(dst) && !is_host_ptr(src)) {
-    int rc = launch_tma_rows<PACK>(c, dst, src, nd, sizes, strides, elem, s);
+  if (!is_host_ptr(dst) && !is_host_ptr(src)) {
+    int rc = strides[last] == 1 ? launch_tma_rows<PACK>(c, dst, src, nd, sizes, strides, elem, s)
+                                : launch_tma_transpose<PACK>(c, dst, src, nd, sizes, strides, elem, s);
     if (rc <= 0) return rc;
   }
   if (strides[last] == 1) {
@@ -982,9 +1087,39 @@ int launch_zvc_decode(lms_ctx* c, const char* enc, uint64_t nwords, uint32_t* ds
   return LMS_OK;
 }
 
+// timing keeps the most recent transfers only: past kMaxRecs the oldest
+// finished half is dropped (their events go back to the pool) and the record
+// indices handles hold are invalidated through trace_gen
+constexpr size_t kMaxRecs = size_t(1) << 17;
+
+void trim_records(lms_ctx* c) {
+  size_t k = 0;
+  const size_t half = c->recs.size() / 2;
+  while (k < half && cudaEventQuery(c->recs[k].end) == cudaSuccess) ++k;
+  if (k == 0) return;
+  for (size_t i = 0; i < k; ++i) {
+    c->events.put(c->recs[i].start, true);
+    c->events.put(c->recs[i].end, true);
+  }
+  c->recs.erase(c->recs.begin(), c->recs.begin() + k);
+  size_t w = 0;
+  for (size_t i = 0; i < c->waits.size(); ++i) {
+    auto wt = c->waits[i];
+    if (wt.second < int64_t(k)) {
+      c->events.put(wt.first, true);
+      continue;
+    }
+    wt.second -= int64_t(k);
+    c->waits[w++] = wt;
+  }
+  c->waits.resize(w);
+  c->trace_gen++;
+}
+
 void timing_begin(lms_ctx* c, cudaStream_t s, cudaEvent_t* start) {
   *start = nullptr;
   if (!c->cfg.timing) return;
+  if (c->recs.size() >= kMaxRecs) trim_records(c);
   *start = c->events.get(true);
   cudaEventRecord(*start, s);
 }
@@ -1035,6 +1170,14 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
   if (const char* v = getenv("LMS_TMA_PACK")) c->use_tma_pack = atoi(v) != 0;
   cudaFuncSetAttribute(tma_copy_kernel<kTmaStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kTmaStages * int(kTmaBoxTarget) * 2);
+  cudaFuncSetAttribute(tma_transpose_kernel<1, tt_warps<1>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(tma_transpose_smem<1>()));
+  cudaFuncSetAttribute(tma_transpose_kernel<2, tt_warps<2>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(tma_transpose_smem<2>()));
+  cudaFuncSetAttribute(tma_transpose_kernel<4, tt_warps<4>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(tma_transpose_smem<4>()));
+  cudaFuncSetAttribute(tma_transpose_kernel<8, tt_warps<8>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(tma_transpose_smem<8>()));
   cudaFuncSetAttribute(zvc_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
   cudaFuncSetAttribute(zvc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
   int lo = 0, hi = 0;
@@ -1548,7 +1691,7 @@ int lms_swap_wait(lms_ctx* c, lms_handle* h, void* consumer_stream) {
   if (!c || !h) return fail(LMS_E_INVALID, "null argument");
   std::lock_guard<std::mutex> g(c->mu);
   if (!h->in_ready) return fail(LMS_E_STATE, "swap_wait before swap_in");
-  if (c->cfg.timing && h->rec_in >= 0) {
+  if (c->cfg.timing && h->rec_in >= 0 && h->rec_gen == c->trace_gen) {
     cudaEvent_t reach = c->events.get(true);
     CK(cudaEventRecord(reach, static_cast<cudaStream_t>(consumer_stream)));
     c->waits.push_back({reach, h->rec_in});

@@ -71,11 +71,17 @@ def main():
     x = torch.randn(B, C, 56, 56, device=dev)
     tb = x.numel() * 4
     if on("pack"):
-        v = x.permute(0, 2, 3, 1)            # strided: unit stride on C (not last)
+        v = x.permute(0, 2, 3, 1)            # strided: unit stride on W (not last)
         out = torch.empty(v.shape, device=dev)
         t = timed(lambda: ctx.pack(v, out))
         assert torch.equal(out, v.contiguous())
-        res["pack_transpose"] = {"gbs": 2 * tb / t / 1e9, "frac_hbm": 2 * tb / t / 1e9 / hbm_peak, "ms": t * 1e3}
+        res["pack_transpose_tma"] = {"gbs": 2 * tb / t / 1e9, "frac_hbm": 2 * tb / t / 1e9 / hbm_peak,
+                                     "ms": t * 1e3}
+        ctx.set_tuning(0, -1, 0)
+        t = timed(lambda: ctx.pack(v, out))
+        res["pack_transpose_simt"] = {"gbs": 2 * tb / t / 1e9, "frac_hbm": 2 * tb / t / 1e9 / hbm_peak,
+                                      "ms": t * 1e3}
+        ctx.set_tuning(0, -1, 1)
         vs = x[:, :, :, 4:52]                # rows path (unit-stride last dim, 192 B rows)
         outs = torch.empty(vs.shape, device=dev)
         b2 = vs.numel() * 4
@@ -107,7 +113,8 @@ def main():
         src = x.contiguous()
         t = timed(lambda: ctx.unpack(src, v))
         assert torch.equal(v, src)
-        res["unpack_transpose"] = {"gbs": 2 * tb / t / 1e9, "frac_hbm": 2 * tb / t / 1e9 / hbm_peak, "ms": t * 1e3}
+        res["unpack_transpose_tma"] = {"gbs": 2 * tb / t / 1e9, "frac_hbm": 2 * tb / t / 1e9 / hbm_peak,
+                                       "ms": t * 1e3}
         big = torch.empty(B, 2 * C, 56, 56, device=dev)
         vd = big[:, 16:16 + C]                # unpack into a channel slice (TMA store path)
         t = timed(lambda: ctx.unpack(src, vd))

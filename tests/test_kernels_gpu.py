@@ -40,6 +40,12 @@ def _views(dtype):
     wide = (torch.randn(3, 40, 56, 56, device=dev).to(dtype) if dtype.is_floating_point
             else torch.randint(-9, 9, (3, 40, 56, 56), device=dev, dtype=dtype))
     yield "tma_odd_box_bytes", wide[:, :, :, 4:52]   # 192 B rows: boxes not a multiple of 128 B
+    # channels-last views of NCHW tensors: the TMA transpose path (128 B-swizzled tiles)
+    yield "tma_nhwc", big.permute(0, 2, 3, 1)
+    yield "tma_nhwc_batch_slice", big[1:, :, 2:22, :].permute(0, 2, 3, 1)
+    odd = (torch.randn(2, 40, 12, 48, device=dev).to(dtype) if dtype.is_floating_point
+           else torch.randint(-9, 9, (2, 40, 12, 48), device=dev, dtype=dtype))
+    yield "tma_nhwc_partial_tiles", odd.permute(0, 2, 3, 1)
 
 
 @pytest.mark.parametrize("tma", [1, 0])
