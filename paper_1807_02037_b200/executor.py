@@ -302,6 +302,14 @@ def execute(g: CompGraph, inputs: dict, cfg: ExecConfig = ExecConfig(), ctx: rt.
     return out, report
 
 
+def interpret(g: CompGraph, inputs: dict, ctx: rt.Context | None = None) -> dict:
+    """Drop-in for the reference's ``interpret(g, inputs)`` (interp.py:58-163): the
+    same ``{variable name: float64 ndarray}`` result, computed on the GPU in float64
+    by :func:`execute` (swap nodes move real bytes through liblms)."""
+    out, _ = execute(g, inputs, ExecConfig(dtype="float64", return_numpy=True), ctx=ctx)
+    return out
+
+
 def _apply(node, args, torch):
     name = node.name
 

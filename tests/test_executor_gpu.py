@@ -96,3 +96,17 @@ def test_report_schema(lms_ctx):
     kinds = {e["event"] for e in d["event_trace"]}
     assert kinds == {"xfer_start", "xfer_finish"}
     assert rep.peak_host_bytes > 0
+
+
+def test_interpret_dropin_matches_reference_outputs(lms_ctx, interp_cases):
+    """``interpret`` keeps the reference signature (interp.py:58) and its float64
+    results (golden outputs produced by the reference itself)."""
+    from paper_1807_02037_b200 import interpret
+    for case in interp_cases:
+        inputs = {k: np.asarray(v) for k, v in case["inputs"].items()}
+        want = {k: np.asarray(v) for k, v in case["outputs"].items()}
+        for rw in case["rewritten"][:1]:
+            got = interpret(graph_from_dict(rw["graph"]), inputs, ctx=lms_ctx)
+            assert set(got) == set(want)
+            for k in want:
+                assert np.allclose(got[k], want[k], rtol=1e-12, atol=1e-12), (case["name"], k)
