@@ -132,6 +132,9 @@ int lms_dev_free(lms_ctx* ctx, void* ptr, void* stream);
  * `stream` completes (a pending outbound transfer), like sim.py:205-211
  * "free after transfers done" */
 int lms_dev_hold_until(lms_ctx* ctx, const void* ptr, void* stream);
+/* the block containing ptr is also used on `stream` (PyTorch's recordStream):
+ * when it is freed, its reuse waits for the work then enqueued on `stream` */
+int lms_dev_record_stream(lms_ctx* ctx, const void* ptr, void* stream);
 /* storage layout the swap-in restores by default: strides (elements) and the
  * number of storage elements to allocate */
 int lms_handle_layout(lms_handle* h, int64_t* strides_out, int64_t* storage_elems);

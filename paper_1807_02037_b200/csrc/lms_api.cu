@@ -154,6 +154,7 @@ struct lms_ctx {
   uint64_t n_reclaims = 0, n_device_syncs = 0;
   size_t mapped_peak = 0;
   std::unordered_map<char*, std::vector<SharedEv*>> holds;  // block base -> pending readers
+  std::unordered_map<char*, std::vector<void*>> rec_streams;  // block base -> extra streams using it
   std::vector<DevBlk> deferred;                             // freed, waiting for their holds
   size_t deferred_bytes = 0;
 
@@ -453,6 +454,21 @@ int plan_alloc(lms_ctx* c, size_t rsize, void* stream, void** out) {
   return LMS_OK;
 }
 
+// a freed block recorded on other streams is held until the work enqueued
+// there by now completes (the CUDA caching allocator's recordStream rule)
+void apply_recorded_streams(lms_ctx* c, char* base) {
+  auto it = c->rec_streams.find(base);
+  if (it == c->rec_streams.end()) return;
+  for (void* s : it->second) {
+    auto* ev = new SharedEv();
+    ev->e = c->events.get();
+    ev->refs = 1;
+    cudaEventRecord(ev->e, static_cast<cudaStream_t>(s));
+    c->holds[base].push_back(ev);
+  }
+  c->rec_streams.erase(it);
+}
+
 void plan_free(lms_ctx* c, void* ptr, void* stream) {
   auto& P = c->plan;
   const size_t off = static_cast<char*>(ptr) - P.base;
@@ -460,6 +476,7 @@ void plan_free(lms_ctx* c, void* ptr, void* stream) {
   if (it == P.live.end()) return;
   const size_t size = it->second.first;
   const size_t item = it->second.second;
+  apply_recorded_streams(c, static_cast<char*>(ptr));
   P.live.erase(it);
   P.live_bytes -= size;
   bool released = true;
@@ -577,6 +594,7 @@ int dev_free_locked(lms_ctx* c, void* ptr, void* stream) {
   }
   DevBlk d;
   if (!find_dev(c, ptr, true, &d)) return fail(LMS_E_INVALID, "lms_dev_free: not a live allocation");
+  apply_recorded_streams(c, d.base);
   d.stream = stream;
   d.seq = c->vmm->clocks_.stamp(stream);
   c->st.n_free++;
@@ -1485,6 +1503,17 @@ int lms_plan_solve(const uint64_t* sizes, const int64_t* t_alloc, const int64_t*
   }
   *region = plan_place(it);
   for (size_t i = 0; i < n; ++i) offsets[i] = it[i].planned ? it[i].off : UINT64_MAX;
+  return LMS_OK;
+}
+
+int lms_dev_record_stream(lms_ctx* c, const void* ptr, void* stream) {
+  if (!c || !ptr) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!c->vmm || !c->vmm->owns(ptr)) return LMS_OK;
+  DevBlk d;
+  if (!find_dev(c, ptr, false, &d)) return fail(LMS_E_INVALID, "lms_dev_record_stream: pointer not in a live block");
+  auto& v = c->rec_streams[d.base];
+  if (std::find(v.begin(), v.end(), stream) == v.end()) v.push_back(stream);
   return LMS_OK;
 }
 

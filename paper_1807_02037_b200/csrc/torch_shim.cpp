@@ -7,6 +7,7 @@
 // smaller workspace instead of failing the step.
 #include <c10/util/Exception.h>
 #include <cuda_runtime.h>
+#include <torch/csrc/cuda/CUDAPluggableAllocator.h>
 
 #include "../../include/lms.h"
 
@@ -28,4 +29,18 @@ extern "C" void lms_torch_free(void* ptr, size_t size, int device, cudaStream_t 
   (void)device;
   lms_ctx* c = lms_get_global();
   if (c) lms_dev_free(c, ptr, stream);
+}
+
+// Tensor.record_stream(s) on a block of ours: hold its reuse for `s`'s work
+// (ProcessGroupNCCL and other multi-stream code rely on it).  Called once
+// after change_current_allocator installed this shim.
+extern "C" int lms_torch_hook_record_stream() {
+  auto a = torch::cuda::CUDAPluggableAllocator::getCurrentAllocator();
+  auto p = std::dynamic_pointer_cast<torch::cuda::CUDAPluggableAllocator::CUDAPluggableAllocator>(a);
+  if (!p) return -1;
+  p->set_record_stream_fn([](void* ptr, cudaStream_t stream) {
+    lms_ctx* c = lms_get_global();
+    if (c) lms_dev_record_stream(c, ptr, stream);
+  });
+  return 0;
 }

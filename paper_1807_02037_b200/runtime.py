@@ -101,7 +101,7 @@ def lib():
         "lms_plan_solve": ([ctypes.POINTER(ctypes.c_uint64), i64p, i64p, sz, ctypes.POINTER(ctypes.c_uint64),
                             ctypes.POINTER(ctypes.c_uint64)], i),
         "lms_dev_alloc": ([vp, sz, vp, pp], i), "lms_dev_free": ([vp, vp, vp], i),
-        "lms_dev_hold_until": ([vp, vp, vp], i),
+        "lms_dev_hold_until": ([vp, vp, vp], i), "lms_dev_record_stream": ([vp, vp, vp], i),
         "lms_host_alloc": ([vp, sz, pp], i), "lms_host_free": ([vp, vp], i),
         "lms_host_reserve": ([vp, sz], i),
         "lms_swap_out": ([vp, vp, i64p, i64p, i, i, vp, i, pp], i),
@@ -421,6 +421,9 @@ def install_allocator(ctx: Context):
         raise LmsError(f"{SHIM_PATH} is missing; run __graft_entry__.build()")
     alloc = torch.cuda.memory.CUDAPluggableAllocator(SHIM_PATH, "lms_torch_alloc", "lms_torch_free")
     torch.cuda.memory.change_current_allocator(alloc)
+    # Tensor.record_stream on our blocks: reuse waits for the recorded streams
+    if ctypes.CDLL(SHIM_PATH).lms_torch_hook_record_stream() != 0:
+        raise LmsError("could not hook record_stream on the pluggable allocator")
     _installed = ctx
 
 

@@ -77,3 +77,22 @@ def test_budget_is_physical(lms_ctx):
         ctx.dev_free(q)
     finally:
         ctx.close()
+
+
+def test_record_stream_holds_reuse(lms_ctx):
+    """Tensor.record_stream(s) through the pluggable allocator: a block freed on the
+    compute stream is not handed out again before the work queued on `s` ran."""
+    side = torch.cuda.Stream()
+    t = torch.empty(64 * MIB, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(200_000_000)     # keep `side` busy (~0.1 s)
+        t.fill_(3)
+    t.record_stream(side)
+    before = lms_ctx.stats()["n_deferred_frees"]
+    del t
+    st = lms_ctx.stats()
+    assert st["n_deferred_frees"] == before + 1    # held for `side`, not reusable yet
+    torch.cuda.synchronize()
+    lms_ctx.synchronize()
+    assert lms_ctx.stats()["device_deferred_bytes"] == 0
