@@ -338,10 +338,28 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
     return g, meta
 
 
-def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int) -> SwapPlan:
-    """Rewrite the captured graph and map swap-ins back onto pack indices / nodes."""
+def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
+               far_cfg: RewriteConfig | None = None, far_max_fraction: float = 0.0) -> SwapPlan:
+    """Rewrite the captured graph and map swap-ins back onto pack indices / nodes.
+
+    ``far_cfg`` (an extension, not in the reference): a second rewrite of the
+    same graph with only the control-op window changed (e.g. a larger lb);
+    swap-ins of tensors smaller than ``far_max_fraction`` x the largest swapped
+    tensor take their control op from it.  Both rewrites insert the same
+    swap nodes; small tensors start their H2D further ahead of the consumer,
+    big ones keep the memory-lean window.
+    """
     t0 = time.perf_counter()
     out, rep = rewrite(g, cfg)
+    far_ctrl = {}
+    if far_cfg is not None and far_max_fraction > 0:
+        far_out, _ = rewrite(g, far_cfg)
+        ids = {n.id for n in out.nodes if n.kind is NodeKind.SWAP_IN}
+        far_ids = {n.id for n in far_out.nodes if n.kind is NodeKind.SWAP_IN}
+        if ids != far_ids:
+            raise ValueError("far_cfg must differ from cfg only in the control-op window "
+                             "(lb/ub/ctrld_strategy): its swap-ins differ")
+        far_ctrl = {e.dst: e.src for e in far_out.edges if e.action is EdgeAction.CONTROL}
     dt = time.perf_counter() - t0
     tid_to_saved = {tid: si for si, tid in meta["saved_tensor_id"].items()}
     B = meta["B"]
@@ -357,6 +375,7 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int)
     triggers: dict[int, list] = {}
     bwd_start, eager = [], []
     ctrl_of = {e.dst: e.src for e in out.edges if e.action is EdgeAction.CONTROL}
+    biggest = max((s.nbytes for s in saved_info if s.swapped), default=0)
     for n in out.nodes:
         if n.kind is not NodeKind.SWAP_IN:
             continue
@@ -367,6 +386,8 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int)
         consumers = {B[e.dst] for e in out.out_edges(n.id) if e.action is EdgeAction.READ}
         packs = [k for k in meta["saved"][si].packs if meta["consumer_rank"].get(k) in consumers]
         c = ctrl_of.get(n.id)
+        if far_ctrl and meta["saved"][si].nbytes < far_max_fraction * biggest and n.id in far_ctrl:
+            c = far_ctrl[n.id]
         if c is None:
             kind, trig = "eager", None
         elif c in B:
@@ -539,11 +560,13 @@ class LMS:
     """
 
     def __init__(self, model, loss_fn, optimizer, cfg: RewriteConfig, ctx: rt.Context,
-                 codec="ce", min_swap_bytes: int = 1 << 16, static_plan: bool = True):
+                 codec="ce", min_swap_bytes: int = 1 << 16, static_plan: bool = True,
+                 far_cfg: RewriteConfig | None = None, far_max_fraction: float = 0.0):
         self.model, self.loss_fn, self.optimizer = model, loss_fn, optimizer
         # static step plan (include/lms.h): step 0 after a (re)plan runs on the
         # dynamic pool, step 1 is recorded and placed, later steps replay it
         self.static_plan = static_plan
+        self.far_cfg, self.far_max_fraction = far_cfg, far_max_fraction
         self._plan_step = 0
         self._plan_misses = 0
         self.plan_note = None
@@ -570,7 +593,7 @@ class LMS:
         """Re-run the rewrite with new knobs on the captured graph (no re-trace)."""
         self._drop_step_plan()
         self.cfg = cfg
-        self.plan = build_plan(self.graph, self.meta, cfg, 0)
+        self.plan = build_plan(self.graph, self.meta, cfg, 0, self.far_cfg, self.far_max_fraction)
         self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
         return self.plan
 

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--no-trim", action="store_true")
     ap.add_argument("--refine", default="2", help="comma list of steps that refine the plan")
     ap.add_argument("--n-tensors", type=int, default=-1)
+    ap.add_argument("--lb", type=int, default=1)
+    ap.add_argument("--far-lb", type=int, default=0)
+    ap.add_argument("--far-frac", type=float, default=0.0)
     ap.add_argument("--pre", default="", help="comma list of n_tensors: 2 dynamic steps each before the run "
                                             "(what bench.py's fit probes do)")
     args = ap.parse_args()
@@ -58,13 +61,17 @@ def main():
     x = torch.randn(args.batch, 3, 224, 224, device=dev)
     y = torch.randint(0, 1000, (args.batch,), device=dev)
     for n_pre in [int(v) for v in args.pre.split(",") if v]:
-        lms.replan(RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1, n_tensors=n_pre))
+        lms.replan(RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1, n_tensors=n_pre, lb=args.lb))
         lms.static_plan = False
         for _ in range(2):
             lms.step(x, y)
         torch.cuda.synchronize()
     lms.static_plan = not args.no_plan
-    lms.replan(RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1, n_tensors=args.n_tensors))
+    if args.far_lb:
+        lms.far_cfg = RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1, n_tensors=args.n_tensors,
+                                    lb=args.far_lb)
+        lms.far_max_fraction = args.far_frac
+    lms.replan(RewriteConfig(fuse_swapins=True, swapin_fuse_distance=1, n_tensors=args.n_tensors, lb=args.lb))
     del xc, yc
     if args.e2e:
         xh, yh = x.cpu().pin_memory(), y.cpu().pin_memory()

@@ -56,3 +56,23 @@ def test_n_tensors_and_fusion_knobs_apply():
     assert len(pf.groups) <= len(pn.groups)
     pd = build_plan(g, meta, RewriteConfig(ctrld_strategy="direct_order", lb=2), capture_batch=2)
     assert pd.report.control_edges_added > 0
+
+
+def test_far_window_only_moves_small_tensors_triggers():
+    """build_plan(far_cfg=...): same swap-ins as the plain rewrite; tensors under the
+    size fraction take the far rewrite's control op, the rest keep their own."""
+    import pytest
+    m = _model()
+    x = torch.randn(4, 3, 16, 16)
+    y = torch.randint(0, 10, (4,))
+    g, meta = capture_graph(lambda: torch.nn.functional.cross_entropy(m(x), y), min_swap_bytes=0)
+    near = build_plan(g, meta, RewriteConfig(lb=1), 4)
+    far = build_plan(g, meta, RewriteConfig(lb=3), 4)
+    mixed = build_plan(g, meta, RewriteConfig(lb=1), 4, RewriteConfig(lb=3), 0.5)
+    assert [grp.packs for grp in mixed.groups] == [grp.packs for grp in near.groups]
+    biggest = max(s.nbytes for s in near.saved if s.swapped)
+    for a, b, c in zip(near.groups, far.groups, mixed.groups):
+        small = near.saved[a.saved].nbytes < 0.5 * biggest
+        assert (c.trigger, c.trigger_kind) == ((b.trigger, b.trigger_kind) if small else (a.trigger, a.trigger_kind))
+    with pytest.raises(ValueError):   # a far rewrite with other swap-ins is refused
+        build_plan(g, meta, RewriteConfig(lb=1), 4, RewriteConfig(lb=3, n_tensors=1), 0.5)
