@@ -445,9 +445,10 @@ class SwapExecutor:
         self.codec = codec
         self.last_stats = {}
 
-    # ZVC pays off once enough words are zero: its stream is 1/32 bitmask
-    # plus the nonzero words, and it runs on SMs instead of the copy engine
-    ZVC_MIN_ZERO_FRAC = 0.25
+    # ZVC pays off once enough words are zero: its stream is 1/32 bitmask plus
+    # the nonzero words, moved by SMs at ~51 GB/s where the copy engine does
+    # ~55.5 (profiles/README.md), so it wins above ~11 % zero words
+    ZVC_MIN_ZERO_FRAC = 0.15
 
     def _codec_for(self, si: int, t) -> str:
         if self.codec == "auto":
