@@ -493,10 +493,15 @@ def main():
     # pinned host chunks are allocated now, not inside timed steps: what the
     # probes needed plus two chunks of headroom, within this rank's share
     ctx.host_reserve(min(host_cap, ctx.stats()["host_reserved"] + 8 * GIB))
-    for n_use in sorted(set(ok_ns)):
+    clk = None
+
+    def run_timed(n_use):
+        """Warm-up + exactly ``args.steps`` timed swapped steps; None if the budget is hit."""
+        nonlocal st0, clk
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
                                  ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
                                  swapin_fuse_distance=args.fuse_distance))
+        clocks = Clocks(local)
         try:
             for _ in range(args.warmup):
                 lms.step(xs, ys)
@@ -504,21 +509,37 @@ def main():
             ctx.trace_clear()
             ctx.reset_peaks()
             st0 = ctx.stats()
-            clocks = Clocks(local)
             clocks.start()
-            swap_ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps, tag="swapped")
+            ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps, tag="swapped")
             clk = clocks.stop()
-            break
+            return ms
         except RuntimeError as e:
             if not is_oom(e):
                 raise
-            log(f"[bench] timed run OOM with n_tensors={n_use}; trying more tensors")
+            if clocks.proc is not None:
+                clocks.stop()
+            log(f"[bench] timed run OOM at batch {bs} with n_tensors={n_use}")
             traceback.clear_frames(e.__traceback__)
             rewrap()
             opt.zero_grad(set_to_none=True)
             gc.collect()
             torch.cuda.synchronize(dev)
             ctx.synchronize()
+            return None
+
+    st0 = None
+    for n_use in sorted(set(ok_ns)):
+        swap_ms = run_timed(n_use)
+        if swap_ms is not None:
+            break
+    for shrink in (0.97, 0.94, 0.9):   # last resort: a slightly smaller batch, every tensor swapped
+        if swap_ms is not None:
+            break
+        xs = ys = None
+        gc.collect()
+        bs = max(b0 if b0 > 0 else 1, int(bs * shrink))
+        xs, ys = batch(bs, seed=7)
+        swap_ms = run_timed(N)
     if swap_ms is None:
         raise SystemExit("swapped run did not fit the budget")
     plan = lms.plan
