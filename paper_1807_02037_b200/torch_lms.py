@@ -444,6 +444,7 @@ class SwapExecutor:
         self.plan = plan
         self.codec = codec
         self.last_stats = {}
+        self.handle_tensor: dict[int, int] = {}   # lms handle id -> captured graph tensor id (last step)
 
     # ZVC pays off once enough words are zero: its stream is 1/32 bitmask plus
     # the nonzero words, moved by SMs at ~51 GB/s where the copy engine does
@@ -492,6 +493,7 @@ class SwapExecutor:
             if h is None:
                 h = ctx.swap_out(t, self._codec_for(si, t), stream_of())
                 handles[si] = h
+                self.handle_tensor[h.id] = plan.saved[si].tid
                 for gid in plan.eager_groups:
                     if plan.groups[gid].saved == si:
                         issue(gid)
@@ -603,6 +605,23 @@ class LMS:
     # recorded step ran on the dynamic pool and is slower than a replay)
     REFINE_STEPS = (2,)
     TRIM_ZOMBIES = 256   # 64 MiB pages: 16 GiB of stale VA
+
+    def trace_events(self):
+        """The last steps' measured transfers as the reference's ``TraceEvent``s
+        (``sim.py:74-81``): ``xfer_start``/``xfer_finish`` per swap, time in
+        seconds from the context epoch, tensor = the captured graph's tensor id,
+        device = where the bytes land.  ``write_trace_csv`` writes them in the
+        reference's CSV schema, so measured and simulated timelines diff."""
+        from .report import TraceEvent
+        ev = []
+        tids = self._exec.handle_tensor if self._exec else {}
+        for r in self.ctx.trace():
+            tid = self.meta["saved_tensor_id"].get(tids.get(r["handle_id"])) if self.meta else None
+            where = "host" if r["direction"] == 0 else f"acc:{self.ctx.device}"
+            ev.append(TraceEvent(r["start_ms"] * 1e-3, "xfer_start", None, tid, r["wire_bytes"], where))
+            ev.append(TraceEvent(r["end_ms"] * 1e-3, "xfer_finish", None, tid, r["wire_bytes"], where))
+        ev.sort(key=lambda e: e.time)
+        return ev
 
     def _drop_step_plan(self):
         if self._plan_step >= 2 or self.plan_note == "region":

@@ -76,3 +76,24 @@ def test_far_window_only_moves_small_tensors_triggers():
         assert (c.trigger, c.trigger_kind) == ((b.trigger, b.trigger_kind) if small else (a.trigger, a.trigger_kind))
     with pytest.raises(ValueError):   # a far rewrite with other swap-ins is refused
         build_plan(g, meta, RewriteConfig(lb=1), 4, RewriteConfig(lb=3, n_tensors=1), 0.5)
+
+
+def test_resnet50_capture_counts():
+    """ResNet-50 (the headline model): every saved activation that outlives its
+    forward op becomes a swap candidate; the rewrite is deterministic."""
+    import torchvision
+    torch.manual_seed(0)
+    m = torchvision.models.resnet50()
+    x = torch.randn(2, 3, 64, 64)
+    y = torch.randint(0, 1000, (2,))
+    persistent = list(m.parameters()) + list(m.buffers()) + [x, y]
+    g, meta = capture_graph(lambda: torch.nn.functional.cross_entropy(m(x), y), 0, persistent)
+    assert validate(g) == []
+    a = build_plan(g, meta, RewriteConfig(fuse_swapins=True), 2)
+    b = build_plan(g, meta, RewriteConfig(fuse_swapins=True), 2)
+    assert a.report.to_dict() == b.report.to_dict()
+    assert a.report.tensors_swapped >= 100          # conv/BN/ReLU activations of 53 convs
+    assert len(a.groups) >= a.report.tensors_swapped
+    assert not a.bwd_start_groups                   # chain_rule finds backward control ops
+    capped = build_plan(g, meta, RewriteConfig(fuse_swapins=True, n_tensors=10), 2)
+    assert capped.report.tensors_swapped == 10

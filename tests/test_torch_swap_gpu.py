@@ -116,5 +116,17 @@ def test_static_plan_replay_matches_plain(lms_ctx, codec):
     assert la == lb
     for pa, pb in zip(base.parameters(), swp.parameters()):
         assert torch.equal(pa, pb)
+    # measured transfers in the reference's TraceEvent / CSV schema (sim.py:74-81)
+    ev = lms.trace_events()
+    graph_tids = {t.id for t in lms.graph.tensors}
+    mine = [e for e in ev if e.tensor is not None]
+    assert mine and all(e.tensor in graph_tids for e in mine)
+    assert {e.event for e in mine} == {"xfer_start", "xfer_finish"}
+    import os
+    import tempfile
+    from paper_1807_02037_b200 import write_trace_csv
+    with tempfile.TemporaryDirectory() as d:
+        write_trace_csv(mine, os.path.join(d, "t.csv"))
+        assert open(os.path.join(d, "t.csv")).readline().strip() == "time,event,node,tensor,bytes"
     lms.replan(lms.cfg)   # drops the plan and returns its region
     assert not lms_ctx.plan_info()["ready"]
