@@ -563,7 +563,7 @@ class LMS:
     """
 
     def __init__(self, model, loss_fn, optimizer, cfg: RewriteConfig, ctx: rt.Context,
-                 codec="ce", min_swap_bytes: int = 1 << 16, static_plan: bool = True,
+                 codec="auto", min_swap_bytes: int = 1 << 16, static_plan: bool = True,
                  far_cfg: RewriteConfig | None = None, far_max_fraction: float = 0.0):
         self.model, self.loss_fn, self.optimizer = model, loss_fn, optimizer
         # static step plan (include/lms.h): step 0 after a (re)plan runs on the
