@@ -55,7 +55,9 @@ def parse():
     ap.add_argument("--strategy", default="chain_rule")
     ap.add_argument("--fuse-swapins", action="store_true", default=True)
     ap.add_argument("--no-fuse-swapins", dest="fuse_swapins", action="store_false")
-    ap.add_argument("--fuse-distance", type=int, default=1, help="RewriteConfig.swapin_fuse_distance")
+    ap.add_argument("--fuse-distance", type=int, default=12,
+                    help="RewriteConfig.swapin_fuse_distance (12: a tensor read by two backward ops "
+                         "a few levels apart is swapped in once)")
     ap.add_argument("--b0", type=int, default=0, help="skip bisection and use this no-swap batch")
     ap.add_argument("--n-tensors", type=int, default=0,
                     help="swap only the first n candidate tensors (rewrite BFS order); -1 = all; "
