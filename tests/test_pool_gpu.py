@@ -96,3 +96,55 @@ def test_record_stream_holds_reuse(lms_ctx):
     torch.cuda.synchronize()
     lms_ctx.synchronize()
     assert lms_ctx.stats()["device_deferred_bytes"] == 0
+
+
+def test_plan_record_replay_refine_keeps_data(lms_ctx):
+    """A synthetic 'step' (fixed sequence of allocations and frees, some blocks held
+    by in-flight side-stream work like swap-out copies) run dynamically, recorded,
+    refined and replayed: every live block keeps its own bytes in every mode."""
+    import random
+    ctx = rt.Context(device=0, device_reserve=768 * MIB, timing=False)
+    side = torch.cuda.Stream()
+    rng = random.Random(7)
+    seq = []                  # ("a", slot, size) / ("f", slot, hold)
+    live = []
+    for i in range(160):
+        if live and (rng.random() < 0.45 or len(live) > 12):
+            k = live.pop(rng.randrange(len(live)))
+            seq.append(("f", k, rng.random() < 0.3))
+        else:
+            seq.append(("a", i, rng.choice([1, 3, 8, 24, 40]) * MIB + rng.randrange(0, 4096, 512)))
+            live.append(i)
+    for k in live:
+        seq.append(("f", k, False))
+    try:
+        modes = [None, rt.PLAN_RECORD, rt.PLAN_REFINE, rt.PLAN_REPLAY, rt.PLAN_REPLAY]
+        for step, mode in enumerate(modes):
+            if mode is not None:
+                ctx.plan_begin(mode)
+            blocks = {}
+            for op, k, x in seq:
+                if op == "a":
+                    p = ctx.dev_alloc(x)
+                    _view(p, x).fill_((k * 7 + step) % 251)
+                    blocks[k] = (p, x)
+                else:
+                    p, n = blocks.pop(k)
+                    assert bool((_view(p, n) == (k * 7 + step) % 251).all()), (step, mode, k)
+                    if x:   # a copy still reading it: the block is held until `side` passes
+                        side.wait_stream(torch.cuda.current_stream())
+                        with torch.cuda.stream(side):
+                            torch.cuda._sleep(2_000_000)
+                        ctx.hold_until(_view(p, n), side)
+                    ctx.dev_free(p)
+            torch.cuda.synchronize()
+            if mode is not None:
+                ctx.plan_end()
+            if mode == rt.PLAN_RECORD:
+                assert ctx.plan_info()["ready"]
+        info = ctx.plan_info()
+        assert info["hits"] > 0 and info["diverged_steps"] == 0
+        ctx.plan_reset()
+    finally:
+        torch.cuda.synchronize()
+        ctx.close()
