@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--tf32", action="store_true")
     ap.add_argument("--same-batch", type=int, default=1,
                     help="also time TFLMS (every candidate swapped) at B0 against the plain step at B0")
+    ap.add_argument("--autotune", action="store_true",
+                    help="pick lb empirically (LMS.autotune over 1,2,3,5,8) before the timed run")
     ap.add_argument("--ddp", action="store_true",
                     help="wrap the model in DistributedDataParallel even at one rank (exercises the DP path)")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
@@ -530,6 +532,16 @@ def main():
             return None
 
     st0 = None
+    if args.autotune:   # empirical control-op window (LMS.autotune); the timed run uses the winner
+        n0 = min(ok_ns)
+        lms.replan(RewriteConfig(n_tensors=n0 if n0 < N else -1, lb=args.lb, ub=args.ub,
+                                 ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
+                                 swapin_fuse_distance=args.fuse_distance))
+        lms.static_plan = False
+        tune = lms.autotune(xs, ys, lbs=(1, 2, 3, 5, 8), steps=2)
+        lms.static_plan = True
+        args.lb = lms.cfg.lb
+        log(f"[bench] autotune lb -> {args.lb}: {tune}")
     for n_use in sorted(set(ok_ns)):
         swap_ms = run_timed(n_use)
         if swap_ms is not None:

@@ -606,6 +606,37 @@ class LMS:
     REFINE_STEPS = (2,)
     TRIM_ZOMBIES = 256   # 64 MiB pages: 16 GiB of stale VA
 
+    def autotune(self, x, y, lbs=(1, 2, 3, 5, 8), steps: int = 3):
+        """Pick the control-op window empirically (the paper leaves the lb/ub
+        heuristic open): for each lb, run ``steps`` swapped steps
+        at this batch (the last one timed with CUDA events); keep the fastest lb
+        that fits the budget.  Returns ``{lb: ms per step or None (OOM)}``; the
+        model's parameters move by ``len(lbs) * steps`` optimizer steps."""
+        from dataclasses import replace
+        base = self.cfg
+        timings = {}
+        for lb in lbs:
+            self.replan(replace(base, lb=lb, ub=max(base.ub, lb)))
+            try:
+                for _ in range(max(1, steps - 1)):
+                    self.step(x, y)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                self.step(x, y)
+                e1.record()
+                torch.cuda.synchronize()
+                timings[lb] = e0.elapsed_time(e1)
+            except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
+                timings[lb] = None
+                self.optimizer.zero_grad(set_to_none=True)
+                torch.cuda.synchronize()
+                self.ctx.synchronize()
+        fits = {lb: ms for lb, ms in timings.items() if ms is not None}
+        best = min(fits, key=fits.get) if fits else base.lb
+        self.replan(replace(base, lb=best, ub=max(base.ub, best)))
+        return timings
+
     def trace_events(self):
         """The last steps' measured transfers as the reference's ``TraceEvent``s
         (``sim.py:74-81``): ``xfer_start``/``xfer_finish`` per swap, time in

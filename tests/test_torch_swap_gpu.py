@@ -130,3 +130,19 @@ def test_static_plan_replay_matches_plain(lms_ctx, codec):
         assert open(os.path.join(d, "t.csv")).readline().strip() == "time,event,node,tensor,bytes"
     lms.replan(lms.cfg)   # drops the plan and returns its region
     assert not lms_ctx.plan_info()["ready"]
+
+
+def test_autotune_picks_a_fitting_window(lms_ctx):
+    """LMS.autotune tries control-op windows and keeps the fastest that fits."""
+    torch.backends.cudnn.benchmark = False
+    net = _net()
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(32, 3, 32, 32, device="cuda", generator=gen)
+    y = torch.randint(0, 10, (32,), device="cuda", generator=gen)
+    lms = LMS(net, torch.nn.functional.cross_entropy, torch.optim.SGD(net.parameters(), lr=0.01),
+              RewriteConfig(fuse_swapins=True), lms_ctx, min_swap_bytes=0)
+    lms.capture(x[:4], y[:4])
+    t = lms.autotune(x, y, lbs=(1, 3), steps=2)
+    assert set(t) == {1, 3} and all(v is not None and v > 0 for v in t.values())
+    assert lms.cfg.lb == min(t, key=t.get)
+    assert float(lms.step(x, y).detach()) > 0
