@@ -208,9 +208,10 @@ def main():
 
     # the pool must own PyTorch's allocator before anything lazily initialises CUDA
     # pinned host memory is shared by the ranks of this box: each gets its share
-    # (80 % of MemAvailable / local ranks), enforced by the host pool
+    # (60 % of MemAvailable / local ranks, less 4 GiB for the process itself),
+    # enforced by the host pool so the box never pages or OOM-kills
     local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", ws))
-    host_cap = int(0.8 * host_available() / max(1, local_ws))
+    host_cap = max(1 * GIB, int(0.6 * host_available() / max(1, local_ws)) - 4 * GIB)
     ctx = rt.Context(device=local, device_reserve=budget, host_chunk=4 * GIB, timing=True, host_limit=host_cap)
     rt.install_allocator(ctx)
     torch.cuda.set_device(local)
