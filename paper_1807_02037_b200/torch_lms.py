@@ -671,7 +671,13 @@ class LMS:
                     else rt.PLAN_REPLAY if self._plan_step >= 2 else rt.PLAN_OFF)
         if mode == rt.PLAN_RECORD:
             torch.cuda.synchronize()
-            self.ctx.plan_reset()       # a plan left over from a failed step
+            try:
+                self.ctx.plan_reset()   # a plan left over from a failed step
+            except rt.LmsError:
+                # blocks of the failed step's plan are still referenced: run this
+                # step on the dynamic pool and record the next one
+                mode = rt.PLAN_OFF
+                self._plan_step = 0
         if mode != rt.PLAN_OFF:
             self.ctx.plan_begin(mode)
         try:
