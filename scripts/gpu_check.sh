@@ -7,4 +7,4 @@ nvidia-smi topo -m > gpurun_out/topo.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout ${BENCH_TIMEOUT:-1200} python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.log; echo "bench rc=$?" >> gpurun_out/bench.log
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -5 gpurun_out/bench.log; cat gpurun_out/bench.json
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -5 gpurun_out/bench.log; cat gpurun_out/bench.json
