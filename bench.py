@@ -70,6 +70,8 @@ def parse():
                     help="also time TFLMS (every candidate swapped) at B0 against the plain step at B0")
     ap.add_argument("--autotune", action="store_true",
                     help="pick lb empirically (LMS.autotune over 1,2,3,5,8) before the timed run")
+    ap.add_argument("--tune-windows", type=int, default=0,
+                    help="memory-aware per-swap-in control ops (LMS.tune_windows) before the timed run")
     ap.add_argument("--ddp", action="store_true",
                     help="wrap the model in DistributedDataParallel even at one rank (exercises the DP path)")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
@@ -500,14 +502,20 @@ def main():
     ctx.host_reserve(min(host_cap, ctx.stats()["host_reserved"] + 8 * GIB))
     clk = None
 
-    def run_timed(n_use):
+    tuned = {}
+
+    def run_timed(n_use, tune=False):
         """Warm-up + exactly ``args.steps`` timed swapped steps; None if the budget is hit."""
-        nonlocal st0, clk
+        nonlocal st0, clk, tuned
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
                                  ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
                                  swapin_fuse_distance=args.fuse_distance))
         clocks = Clocks(local)
+        tuned = {}
         try:
+            if tune:
+                tuned = lms.tune_windows(xs, ys)
+                log(f"[bench] tune_windows: {tuned}")
             for _ in range(args.warmup):
                 lms.step(xs, ys)
             torch.cuda.synchronize(dev)
@@ -544,7 +552,10 @@ def main():
         args.lb = lms.cfg.lb
         log(f"[bench] autotune lb -> {args.lb}: {tune}")
     for n_use in sorted(set(ok_ns)):
-        swap_ms = run_timed(n_use)
+        for tune in ((True, False) if args.tune_windows else (False,)):
+            swap_ms = run_timed(n_use, tune)
+            if swap_ms is not None:
+                break
         if swap_ms is not None:
             break
     for shrink in (0.97, 0.94, 0.9):   # last resort: a slightly smaller batch, every tensor swapped
@@ -692,7 +703,7 @@ def main():
                  "device_peak_bytes": st1["device_peak"], "host_peak_bytes": st1["host_peak"],
                  "attempts": attempts, "capture_s": round(capture_s, 2),
                  "rewrite_s": round(plan.rewrite_seconds, 3), "bisect_s": round(bisect_s, 1),
-                 "graph_nodes": len(lms.graph.nodes), "static_plan": lms.plan_note,
+                 "graph_nodes": len(lms.graph.nodes), "static_plan": lms.plan_note, "tune_windows": tuned,
                  "timed_host_grows": st1["n_host_grow"] - st0["n_host_grow"],
                  "timed_host_grow_ms": round(st1["host_grow_ms"] - st0["host_grow_ms"], 1),
                  "timed_page_moves": st1["n_reclaims"] - st0["n_reclaims"],

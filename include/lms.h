@@ -169,6 +169,9 @@ typedef struct {
   uint64_t refinements;    /* REFINE steps whose re-placement was adopted */
 } lms_plan_info_t;
 int lms_plan_info(lms_ctx* ctx, lms_plan_info_t* out);
+/* the recording step's event clock so far (-1 outside RECORD): lets a caller
+ * place its own host events (e.g. a control op firing) on the items' clock */
+int lms_plan_clock(lms_ctx* ctx, int64_t* out);
 /* the recorded step (after lms_plan_end of a RECORD step): up to `cap` items */
 int lms_plan_items(lms_ctx* ctx, uint64_t* sizes, int64_t* t_alloc, int64_t* t_free, int64_t* t_free_logical,
                    size_t cap, size_t* n);

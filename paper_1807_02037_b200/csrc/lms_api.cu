@@ -1453,6 +1453,13 @@ int lms_plan_reset(lms_ctx* c) {
   return LMS_OK;
 }
 
+int lms_plan_clock(lms_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(LMS_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> g(c->mu);
+  *out = c->plan.mode == LMS_PLAN_RECORD ? c->plan.clock : -1;
+  return LMS_OK;
+}
+
 int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
   if (!c || !out) return fail(LMS_E_INVALID, "null argument");
   std::lock_guard<std::mutex> g(c->mu);

@@ -97,6 +97,7 @@ def lib():
         "lms_set_tuning": ([vp, i, i, i], i),
         "lms_plan_begin": ([vp, i], i), "lms_plan_end": ([vp], i), "lms_plan_reset": ([vp], i),
         "lms_plan_info": ([vp, ctypes.POINTER(_PlanInfo)], i),
+        "lms_plan_clock": ([vp, i64p], i),
         "lms_plan_items": ([vp, ctypes.POINTER(ctypes.c_uint64), i64p, i64p, i64p, sz, ctypes.POINTER(sz)], i),
         "lms_plan_solve": ([ctypes.POINTER(ctypes.c_uint64), i64p, i64p, sz, ctypes.POINTER(ctypes.c_uint64),
                             ctypes.POINTER(ctypes.c_uint64)], i),
@@ -240,6 +241,12 @@ class Context:
         n = ctypes.c_size_t()
         _check(lib().lms_plan_items(self.ptr, u64, a, b, lg, cap, ctypes.byref(n)), "lms_plan_items")
         return [(u64[i], a[i], b[i], lg[i]) for i in range(min(cap, n.value))]
+
+    def plan_clock(self) -> int:
+        """The recording step's event clock (items' t_alloc/t_free units); -1 outside RECORD."""
+        v = ctypes.c_int64()
+        _check(lib().lms_plan_clock(self.ptr, ctypes.byref(v)), "lms_plan_clock")
+        return v.value
 
     def plan_reset(self):
         _check(lib().lms_plan_reset(self.ptr), "lms_plan_reset")

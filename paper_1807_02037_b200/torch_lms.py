@@ -102,6 +102,7 @@ class SwapGroup:
     packs: list                 # pack indices this group serves
     trigger: int | None         # node rank of the control op's backward node; None = eager
     trigger_kind: str           # "backward" | "forward->bwd-start" | "eager"
+    node: int = -1              # the swap-in node's id in the rewritten graph
 
 
 @dataclass
@@ -394,7 +395,7 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
             kind, trig = "backward", B[c]
         else:
             kind, trig = "forward->bwd-start", None
-        grp = SwapGroup(len(groups), si, packs, trig, kind)
+        grp = SwapGroup(len(groups), si, packs, trig, kind, n.id)
         groups.append(grp)
         for k in packs:
             pack_group[k] = grp.gid
@@ -427,6 +428,28 @@ def _issuer(issue, gids):
     return hook
 
 
+def _clocker(ctx, out, rank):
+    def hook(grad_inputs, grad_outputs):
+        out[rank] = ctx.plan_clock()
+        return None
+    return hook
+
+
+def retarget(plan: SwapPlan, moves: dict) -> SwapPlan:
+    """``plan`` with the swap-ins in ``moves`` ({gid: node rank}) fired by other
+    backward nodes; each node issues its swap-ins in their original order."""
+    from dataclasses import replace
+    groups = [replace(g, trigger=moves[g.gid]) if g.gid in moves else g for g in plan.groups]
+    triggers: dict[int, list] = {}
+    for r, gids in plan.triggers.items():   # a node's own swap-ins first, in their order
+        kept = [gid for gid in gids if gid not in moves]
+        if kept:
+            triggers[r] = kept
+    for gid, r in moves.items():            # then the moved ones, in ``moves`` order
+        triggers.setdefault(r, []).append(gid)
+    return replace(plan, groups=groups, triggers=triggers)
+
+
 class _SwapRef:
     """What autograd keeps instead of a swapped tensor."""
 
@@ -445,6 +468,10 @@ class SwapExecutor:
         self.codec = codec
         self.last_stats = {}
         self.handle_tensor: dict[int, int] = {}   # lms handle id -> captured graph tensor id (last step)
+        # window probe (LMS.tune_windows): {"ranks": node ranks to clock} -> the run
+        # fills "node_clock" {rank: plan clock when the node finished on the host}
+        # and "issue" {gid: (plan clock at the swap-in, bytes)}
+        self.probe: dict | None = None
 
     # ZVC pays off once enough words are zero: its stream is 1/32 bitmask plus
     # the nonzero words, moved by SMs at ~51 GB/s where the copy engine does
@@ -468,6 +495,9 @@ class SwapExecutor:
         group_left = {g.gid: len(g.packs) for g in plan.groups}
         issued: set[int] = set()
         stream_of = torch.cuda.current_stream
+        probe = self.probe
+        if probe is not None:
+            probe["node_clock"], probe["issue"] = {}, {}
 
         def issue(gid):
             if gid in issued:
@@ -477,6 +507,8 @@ class SwapExecutor:
             if h is None:
                 return  # its swap-out never happened (structure changed); unpack will fail loudly
             issued.add(gid)
+            if probe is not None:
+                probe["issue"][gid] = (ctx.plan_clock(), h.logical_bytes)
             group_tensor[gid] = ctx.swap_in(h, trigger_stream=stream_of())
 
         def pack(t):
@@ -526,12 +558,15 @@ class SwapExecutor:
                 raise RuntimeError(f"step saved {k_counter[0]} tensors but the plan was captured with "
                                    f"{plan.n_packs}; re-capture the plan for this model/step")
             # hook the control ops of this step's graph
-            if plan.triggers:
+            if plan.triggers or probe is not None:
                 ops = sorted((n for n in _walk(loss.grad_fn) if not _is_accumulate(n)),
                              key=lambda n: n._sequence_nr())
                 seq0 = ops[0]._sequence_nr()
                 for n in ops:
-                    gids = plan.triggers.get(n._sequence_nr() - seq0)
+                    r = n._sequence_nr() - seq0
+                    if probe is not None and r in probe["ranks"]:
+                        hooks.append(n.register_hook(_clocker(ctx, probe["node_clock"], r)))
+                    gids = plan.triggers.get(r)
                     if gids:
                         hooks.append(n.register_hook(_issuer(issue, gids)))
             for gid in plan.bwd_start_groups:
@@ -636,6 +671,90 @@ class LMS:
         best = min(fits, key=fits.get) if fits else base.lb
         self.replan(replace(base, lb=best, ub=max(base.ub, best)))
         return timings
+
+    def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8), margin: float = 0.02) -> dict:
+        """Memory-aware control-op windows, one per swap-in (an extension: the
+        paper leaves choosing lb open).  Every candidate control
+        op comes from the reference's own strategy run with a wider window
+        (``rewrite`` at each lb in ``lbs``, same swap nodes), so each chosen edge
+        is one the rewrite itself could emit.
+
+        One recorded step under the current plan gives the device pool's live
+        bytes on its event clock (``lms_plan_items``) and, for every candidate
+        node, the clock at which it finished on the host (``lms_plan_clock``).
+        Moving a swap-in from clock c1 to an earlier node at c2 keeps its
+        destination live over [c2, c1); swap-ins are visited in issue order and
+        each takes the earliest candidate that keeps the live bytes under the
+        pool's room (less ``margin``) and does not pass the previous swap-in's
+        trigger (the H2D channel stays in consumer order).  The plan is then
+        re-targeted (``retarget``) and re-recorded by the next steps.
+        Returns a summary dict; ``{}`` changes nothing (no room, or no
+        static plan to measure)."""
+        from dataclasses import replace
+        import numpy as np
+        if not self.static_plan or self.plan is None:
+            return {}
+        base = self.cfg
+        B = self.meta["B"]
+        node_of = {g.node: g.gid for g in self.plan.groups if g.trigger_kind == "backward"}
+        cands: dict[int, list] = {gid: [] for gid in node_of.values()}
+        for lb in lbs:
+            out, _ = rewrite(self.graph, replace(base, lb=lb, ub=max(base.ub, lb)))
+            for e in out.edges:
+                if e.action is EdgeAction.CONTROL and e.dst in node_of and e.src in B:
+                    cands[node_of[e.dst]].append(B[e.src])
+        ranks = {r for v in cands.values() for r in v}
+        if not ranks:
+            return {}
+        # step 0 of the plan runs dynamic; step 1 records with the probe on
+        self._drop_step_plan()
+        while self._plan_step != 1:
+            self.step(x, y)
+        self._exec.probe = probe = {"ranks": ranks}
+        try:
+            self.step(x, y)
+        finally:
+            self._exec.probe = None
+        torch.cuda.synchronize()
+        if self.plan_note != "region":
+            return {}
+        info = self.ctx.plan_info()
+        items = self.ctx.plan_items()
+        T = max((max(a, b, c) for _, a, b, c in items), default=0) + 2
+        live = np.zeros(T, dtype=np.float64)
+        for size, a, b, c in items:
+            if b >= 0:
+                live[a:b] += size
+        limit = info["room_bytes"] * (1.0 - margin)
+        start_peak = float(live.max()) if T else 0.0
+        node_clock = probe["node_clock"]
+        issue = sorted(((c, gid, nb) for gid, (c, nb) in probe["issue"].items() if gid in cands))
+        moves, prev, moved_bytes = {}, -1, 0
+        for c1, gid, nb in issue:
+            best = None
+            for r in cands[gid]:
+                c2 = node_clock.get(r)
+                if c2 is None or c2 >= c1 or c2 < prev:
+                    continue
+                if best is not None and c2 >= best[1]:
+                    continue
+                if live[c2:c1].max() + nb <= limit:
+                    best = (r, c2)
+            if best is None:
+                prev = max(prev, c1)
+                continue
+            r, c2 = best
+            live[c2:c1] += nb
+            moves[gid] = r
+            moved_bytes += nb
+            prev = c2
+        if moves:
+            self.plan = retarget(self.plan, moves)
+            self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
+            self._drop_step_plan()
+        return {"moved": len(moves), "of": len(issue), "moved_bytes": moved_bytes,
+                "peak_before": start_peak, "peak_after": float(live.max()), "limit": limit,
+                "lower_bound": info["lower_bound_bytes"]}
 
     def trace_events(self):
         """The last steps' measured transfers as the reference's ``TraceEvent``s

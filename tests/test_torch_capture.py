@@ -97,3 +97,29 @@ def test_resnet50_capture_counts():
     assert not a.bwd_start_groups                   # chain_rule finds backward control ops
     capped = build_plan(g, meta, RewriteConfig(fuse_swapins=True, n_tensors=10), 2)
     assert capped.report.tensors_swapped == 10
+
+
+def test_retarget_moves_triggers_and_keeps_issue_order():
+    """retarget(plan, moves): the moved swap-ins fire from the new node, after that
+    node's own swap-ins; every other group and the packs they serve are unchanged."""
+    from paper_1807_02037_b200.torch_lms import retarget
+    m = _model()
+    x = torch.randn(4, 3, 16, 16)
+    y = torch.randint(0, 10, (4,))
+    g, meta = capture_graph(lambda: torch.nn.functional.cross_entropy(m(x), y), min_swap_bytes=0)
+    near = build_plan(g, meta, RewriteConfig(lb=1), 4)
+    far = build_plan(g, meta, RewriteConfig(lb=3), 4)
+    assert [grp.node for grp in near.groups] == [grp.node for grp in far.groups]
+    moves = {a.gid: b.trigger for a, b in zip(near.groups, far.groups)
+             if a.trigger_kind == b.trigger_kind == "backward" and a.trigger != b.trigger}
+    assert moves, "lb=3 should move at least one control op on this model"
+    out = retarget(near, moves)
+    for a, c in zip(near.groups, out.groups):
+        assert c.packs == a.packs and c.node == a.node
+        assert c.trigger == moves.get(a.gid, a.trigger)
+    flat = sorted(gid for gids in out.triggers.values() for gid in gids)
+    assert flat == sorted(gid for gids in near.triggers.values() for gid in gids)
+    for r, gids in out.triggers.items():
+        own = [gid for gid in near.triggers.get(r, []) if gid not in moves]
+        assert gids[:len(own)] == own
+    assert retarget(near, {}).triggers == near.triggers

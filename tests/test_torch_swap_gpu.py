@@ -146,3 +146,44 @@ def test_autotune_picks_a_fitting_window(lms_ctx):
     assert set(t) == {1, 3} and all(v is not None and v > 0 for v in t.values())
     assert lms.cfg.lb == min(t, key=t.get)
     assert float(lms.step(x, y).detach()) > 0
+
+
+def test_tune_windows_moves_swapins_and_stays_bit_identical(lms_ctx):
+    """LMS.tune_windows: swap-ins re-targeted to earlier control ops from wider
+    windows of the same rewrite (room permitting) still give the plain step's
+    losses and parameters bit for bit, and the re-recorded plan replays."""
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    base = _net()
+    swp = copy.deepcopy(base)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn(5, 32, 3, 32, 32, device="cuda", generator=gen)
+    y = torch.randint(0, 10, (5, 32), device="cuda", generator=gen)
+    loss_fn = torch.nn.functional.cross_entropy
+    opt_a = torch.optim.SGD(base.parameters(), lr=0.1, momentum=0.9)
+
+    def plain(xb, yb):
+        opt_a.zero_grad(set_to_none=True)
+        loss = loss_fn(base(xb), yb)
+        loss.backward()
+        opt_a.step()
+        return loss
+
+    opt_b = torch.optim.SGD(swp.parameters(), lr=0.1, momentum=0.9)
+    lms = LMS(swp, loss_fn, opt_b, RewriteConfig(lb=1), lms_ctx, codec="auto", min_swap_bytes=0)
+    lms.capture(x[0], y[0])
+    before = {g.gid: g.trigger for g in lms.plan.groups}
+    info = lms.tune_windows(x[0], y[0])
+    assert info and info["moved"] > 0 and info["peak_after"] <= info["limit"]
+    moved = [g for g in lms.plan.groups if g.trigger != before[g.gid]]
+    assert len(moved) == info["moved"]
+    # same starting point for both runs
+    swp.load_state_dict(base.state_dict())
+    opt_b.state.clear()
+    la = _train(base, plain, 5, x, y)
+    lb = _train(swp, lms.step, 5, x, y)
+    torch.cuda.synchronize()
+    assert la == lb
+    for pa, pb in zip(base.parameters(), swp.parameters()):
+        assert torch.equal(pa, pb)
+    assert lms.plan_note == "region"
