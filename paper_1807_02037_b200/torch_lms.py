@@ -672,7 +672,7 @@ class LMS:
         self.replan(replace(base, lb=best, ub=max(base.ub, best)))
         return timings
 
-    def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8), margin: float = 0.02) -> dict:
+    def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8, 12, 16, 24, 32, 48), margin: float = 0.02) -> dict:
         """Memory-aware control-op windows, one per swap-in (an extension: the
         paper leaves choosing lb open).  Every candidate control
         op comes from the reference's own strategy run with a wider window

@@ -27,11 +27,14 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--search", type=int, default=6)
     ap.add_argument("--timeout", type=int, default=900)
+    ap.add_argument("--extra", default="", help="more bench.py arguments, e.g. '--tune-windows 1'")
+    ap.add_argument("--tag", default="")
     a = ap.parse_args()
     common = ["--arch", a.arch, "--budget-gib", str(a.budget_gib), "--steps", str(a.steps),
               "--warmup", "3", "--cpu-baseline", "0", "--same-batch", "0", "--search", str(a.search)]
     if a.b0:
         common += ["--b0", str(a.b0)]
+    common += a.extra.split()
     rows = []
     for f in [float(x) for x in a.factors.split(",")]:
         r = run(common + ["--factor", str(f)], a.timeout)
@@ -39,9 +42,9 @@ def main():
         rows.append(r)
         print(json.dumps({k: r.get(k) for k in ("factor", "value", "ms_per_step", "error")}), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"overhead_{a.arch}.json"), "w") as fh:
+    with open(os.path.join(ROOT, "gpurun_out", f"overhead_{a.arch}{a.tag}.json"), "w") as fh:
         json.dump(rows, fh)
-    lines = [f"# {a.arch}: swap overhead vs oversubscription under {a.budget_gib:g} GiB", "",
+    lines = [f"# {a.arch}: swap overhead vs oversubscription under {a.budget_gib:g} GiB {a.extra}", "",
              "overhead = (no-swap img/s at B0) / (swapped img/s at f x B0) - 1, per image", "",
              "| f | batch | tensors swapped / candidates | img/s | ms/step | D2H GB | overhead |",
              "|---|---|---|---|---|---|---|"]
@@ -54,7 +57,7 @@ def main():
         lines.append(f"| {r['factor']} | {r['config']['per_gpu_batch']} | {s['tensors_swapped']} | {r['value']} | "
                      f"{r['ms_per_step']} | {s['d2h_bytes_per_step'] / 1e9:.1f} | {ov:+.1%} |")
     md = "\n".join(lines) + "\n"
-    with open(os.path.join(ROOT, "gpurun_out", f"overhead_{a.arch}.md"), "w") as fh:
+    with open(os.path.join(ROOT, "gpurun_out", f"overhead_{a.arch}{a.tag}.md"), "w") as fh:
         fh.write(md)
     print(md)
 
