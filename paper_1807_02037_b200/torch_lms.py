@@ -672,7 +672,7 @@ class LMS:
         self.replan(replace(base, lb=best, ub=max(base.ub, best)))
         return timings
 
-    def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8, 12, 16, 24, 32, 48), margin: float = 0.02) -> dict:
+    def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8, 12, 16, 24, 32, 48, 64, 96), margin: float = 0.02) -> dict:
         """Memory-aware control-op windows, one per swap-in (an extension: the
         paper leaves choosing lb open).  Every candidate control
         op comes from the reference's own strategy run with a wider window
@@ -729,12 +729,12 @@ class LMS:
         start_peak = float(live.max()) if T else 0.0
         node_clock = probe["node_clock"]
         issue = sorted(((c, gid, nb) for gid, (c, nb) in probe["issue"].items() if gid in cands))
-        moves, prev, moved_bytes = {}, -1, 0
+        moves, prev, moved = {}, -1, []
         for c1, gid, nb in issue:
             best = None
             for r in cands[gid]:
                 c2 = node_clock.get(r)
-                if c2 is None or c2 >= c1 or c2 < prev:
+                if r == self.plan.groups[gid].trigger or c2 is None or c2 >= c1 or c2 < prev:
                     continue
                 if best is not None and c2 >= best[1]:
                     continue
@@ -746,15 +746,50 @@ class LMS:
             r, c2 = best
             live[c2:c1] += nb
             moves[gid] = r
-            moved_bytes += nb
+            moved.append((gid, c1, c2, nb))
             prev = c2
+        # the live bytes bound the placement from below only: keep the longest
+        # prefix of the moves (in issue order) whose recorded step, with those
+        # destinations allocated at their new clocks, still places inside the
+        # room (the pool's own solver, lms_plan_solve; the region the plan
+        # would need is what decides whether replay works)
+        sizes = [it[0] for it in items]
+        t0 = [it[1] for it in items]
+        t1 = [it[2] for it in items]
+        item_at = {a: i for i, a in enumerate(t0)}
+        # a move is modelled only if its destination is the allocation made at
+        # its issue clock (same bytes up to the pool's rounding)
+        moved = [m for m in moved if m[1] in item_at and 0 <= sizes[item_at[m[1]]] - m[3] < (4 << 20)]
+
+        def region_with(k):
+            tk = list(t0)
+            for gid, c1, c2, nb in moved[:k]:
+                i = item_at.get(c1)
+                if i is not None:
+                    tk[i] = c2
+            return rt.plan_solve(sizes, tk, t1)[1]
+
+        keep = len(moved)
+        region = region_with(keep) if moved else 0
+        if moved and region > limit:
+            lo, hi = 0, keep      # lo fits (the recorded plan), hi does not
+            while hi - lo > 1:
+                mid = (lo + hi) // 2
+                if region_with(mid) <= limit:
+                    lo = mid
+                else:
+                    hi = mid
+            keep = lo
+            region = region_with(keep) if keep else info["solved_bytes"]
+        moves = {gid: moves[gid] for gid, *_ in moved[:keep]}
+        moved_bytes = sum(nb for *_, nb in moved[:keep])
         if moves:
             self.plan = retarget(self.plan, moves)
             self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
             self._drop_step_plan()
         return {"moved": len(moves), "of": len(issue), "moved_bytes": moved_bytes,
-                "peak_before": start_peak, "peak_after": float(live.max()), "limit": limit,
-                "lower_bound": info["lower_bound_bytes"]}
+                "candidates": len(moved), "peak_before": start_peak, "region": region,
+                "limit": limit, "lower_bound": info["lower_bound_bytes"]}
 
     def trace_events(self):
         """The last steps' measured transfers as the reference's ``TraceEvent``s

@@ -174,7 +174,7 @@ def test_tune_windows_moves_swapins_and_stays_bit_identical(lms_ctx):
     lms.capture(x[0], y[0])
     before = {g.gid: g.trigger for g in lms.plan.groups}
     info = lms.tune_windows(x[0], y[0])
-    assert info and info["moved"] > 0 and info["peak_after"] <= info["limit"]
+    assert info and info["moved"] > 0 and info["region"] <= info["limit"]
     moved = [g for g in lms.plan.groups if g.trigger != before[g.gid]]
     assert len(moved) == info["moved"]
     # same starting point for both runs
