@@ -1473,7 +1473,7 @@ int lms_plan_info(lms_ctx* c, lms_plan_info_t* out) {
   r.refinements = P.refinements;
   {
     const size_t lp = c->vmm ? c->vmm->live_pages() : 0, tp = c->vmm ? c->vmm->limit_pages() : 0;
-    r.room_bytes = tp > lp ? uint64_t(tp - lp) * c->vmm->page() + (P.region ? P.size : 0) : 0;
+    r.room_bytes = (tp > lp ? uint64_t(tp - lp) * c->vmm->page() : 0) + (P.region ? P.size : 0);
   }
   r.n_items = P.items.size();
   for (auto& it : P.items) r.n_planned += it.planned;

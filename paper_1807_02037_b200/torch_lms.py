@@ -672,7 +672,8 @@ class LMS:
         self.replan(replace(base, lb=best, ub=max(base.ub, best)))
         return timings
 
-    def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8, 12, 16, 24, 32, 48, 64, 96), margin: float = 0.02) -> dict:
+    def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8, 12, 16, 24, 32, 48, 64, 96), margin: float = 0.005,
+                     require_faster: bool = True) -> dict:
         """Memory-aware control-op windows, one per swap-in (an extension: the
         paper leaves choosing lb open).  Every candidate control
         op comes from the reference's own strategy run with a wider window
@@ -686,10 +687,13 @@ class LMS:
         destination live over [c2, c1); swap-ins are visited in issue order and
         each takes the earliest candidate that keeps the live bytes under the
         pool's room (less ``margin``) and does not pass the previous swap-in's
-        trigger (the H2D channel stays in consumer order).  The plan is then
-        re-targeted (``retarget``) and re-recorded by the next steps.
-        Returns a summary dict; ``{}`` changes nothing (no room, or no
-        static plan to measure)."""
+        trigger (the H2D channel stays in consumer order).  The longest prefix
+        of those moves whose placement the pool's solver fits is then tried
+        for real: re-targeted (``retarget``), re-recorded and one replayed step
+        timed against the untouched plan; the set is halved until a replay
+        fits and is faster, or dropped.  The model parameters move by the
+        probe and trial steps (like ``autotune``).  Returns a summary dict;
+        ``{}`` changes nothing (no room, or no static plan to measure)."""
         from dataclasses import replace
         import numpy as np
         if not self.static_plan or self.plan is None:
@@ -725,7 +729,9 @@ class LMS:
         for size, a, b, c in items:
             if b >= 0:
                 live[a:b] += size
-        limit = info["room_bytes"] * (1.0 - margin)
+        # the next recording's room: the pages not live once this plan's region
+        # is returned, less the page the pool keeps for unplanned allocations
+        limit = info["room_bytes"] * (1.0 - margin) - (64 << 20)
         start_peak = float(live.max()) if T else 0.0
         node_clock = probe["node_clock"]
         issue = sorted(((c, gid, nb) for gid, (c, nb) in probe["issue"].items() if gid in cands))
@@ -751,8 +757,7 @@ class LMS:
         # the live bytes bound the placement from below only: keep the longest
         # prefix of the moves (in issue order) whose recorded step, with those
         # destinations allocated at their new clocks, still places inside the
-        # room (the pool's own solver, lms_plan_solve; the region the plan
-        # would need is what decides whether replay works)
+        # room (the pool's own solver, lms_plan_solve)
         sizes = [it[0] for it in items]
         t0 = [it[1] for it in items]
         t1 = [it[2] for it in items]
@@ -764,14 +769,11 @@ class LMS:
         def region_with(k):
             tk = list(t0)
             for gid, c1, c2, nb in moved[:k]:
-                i = item_at.get(c1)
-                if i is not None:
-                    tk[i] = c2
+                tk[item_at[c1]] = c2
             return rt.plan_solve(sizes, tk, t1)[1]
 
         keep = len(moved)
-        region = region_with(keep) if moved else 0
-        if moved and region > limit:
+        if moved and region_with(keep) > limit:
             lo, hi = 0, keep      # lo fits (the recorded plan), hi does not
             while hi - lo > 1:
                 mid = (lo + hi) // 2
@@ -780,16 +782,56 @@ class LMS:
                 else:
                     hi = mid
             keep = lo
-            region = region_with(keep) if keep else info["solved_bytes"]
-        moves = {gid: moves[gid] for gid, *_ in moved[:keep]}
-        moved_bytes = sum(nb for *_, nb in moved[:keep])
-        if moves:
-            self.plan = retarget(self.plan, moves)
-            self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
-            self._drop_step_plan()
-        return {"moved": len(moves), "of": len(issue), "moved_bytes": moved_bytes,
-                "candidates": len(moved), "peak_before": start_peak, "region": region,
+        # the model predicts; a replayed step decides: re-record with the moves,
+        # keep them if the placement fits at the physical-release lifetimes
+        # (alpha 1: no block reused before its swap-out copy landed) and the
+        # replayed step is faster than the untouched plan's; else halve the set
+        orig = self.plan
+        base_ms = self._timed_replay(x, y)
+        trials = {}
+        chosen = 0
+        while keep > 0 and base_ms is not None:
+            self._set_plan(retarget(orig, {gid: moves[gid] for gid, *_ in moved[:keep]}))
+            ms = self._timed_replay(x, y)
+            trials[keep] = ms
+            if ms is not None and (ms < base_ms or not require_faster):
+                chosen = keep
+                break
+            keep //= 2
+        if not chosen:
+            self._set_plan(orig)
+        self._drop_step_plan()
+        return {"moved": chosen, "of": len(issue), "modelled": len(moved),
+                "moved_bytes": sum(nb for *_, nb in moved[:chosen]),
+                "base_ms": base_ms, "trials": trials, "peak_before": start_peak,
                 "limit": limit, "lower_bound": info["lower_bound_bytes"]}
+
+    def _set_plan(self, plan: SwapPlan):
+        self.plan = plan
+        self._exec = SwapExecutor(self.ctx, plan, self.codec)
+        self._drop_step_plan()
+
+    def _timed_replay(self, x, y):
+        """Re-record the current plan and time one replayed step (ms); None if the
+        placement does not fit at physical-release lifetimes or a step hits the budget."""
+        self._drop_step_plan()
+        try:
+            while self._plan_step < 3:
+                self.step(x, y)
+            if self.plan_note != "region" or self.ctx.plan_info()["alpha"] < 1.0:
+                return None
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            self.step(x, y)
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1)
+        except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
+            self.optimizer.zero_grad(set_to_none=True)
+            torch.cuda.synchronize()
+            self.ctx.synchronize()
+            return None
 
     def trace_events(self):
         """The last steps' measured transfers as the reference's ``TraceEvent``s

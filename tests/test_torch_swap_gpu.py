@@ -173,8 +173,8 @@ def test_tune_windows_moves_swapins_and_stays_bit_identical(lms_ctx):
     lms = LMS(swp, loss_fn, opt_b, RewriteConfig(lb=1), lms_ctx, codec="auto", min_swap_bytes=0)
     lms.capture(x[0], y[0])
     before = {g.gid: g.trigger for g in lms.plan.groups}
-    info = lms.tune_windows(x[0], y[0])
-    assert info and info["moved"] > 0 and info["region"] <= info["limit"]
+    info = lms.tune_windows(x[0], y[0], require_faster=False)   # a tiny net: timing is noise
+    assert info and info["moved"] > 0 and info["trials"][info["moved"]] is not None
     moved = [g for g in lms.plan.groups if g.trigger != before[g.gid]]
     assert len(moved) == info["moved"]
     # same starting point for both runs
