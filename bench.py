@@ -71,7 +71,8 @@ def parse():
     ap.add_argument("--autotune", action="store_true",
                     help="pick lb empirically (LMS.autotune over 1,2,3,5,8) before the timed run")
     ap.add_argument("--tune-windows", type=int, default=0,
-                    help="memory-aware per-swap-in control ops (LMS.tune_windows) before the timed run")
+                    help="memory-aware per-swap-in control ops (LMS.tune_windows) before the timed run; "
+                         "2 = also trade swapped-tensor count for prefetch room (tries a few n_tensors)")
     ap.add_argument("--ddp", action="store_true",
                     help="wrap the model in DistributedDataParallel even at one rank (exercises the DP path)")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
@@ -551,6 +552,35 @@ def main():
         lms.static_plan = True
         args.lb = lms.cfg.lb
         log(f"[bench] autotune lb -> {args.lb}: {tune}")
+    joint = None
+    if args.tune_windows >= 2:
+        # more swapped tensors = more link traffic but more room to prefetch:
+        # tune the windows at a few swap-set sizes above the fewest that fit and
+        # keep the fastest replayed step (each candidate's own untouched plan
+        # included)
+        n_min = min(ok_ns)
+        d = max(1, (N - n_min) // 4)
+        cands = sorted({n_min, min(N, n_min + d), min(N, n_min + 2 * d), N})
+        joint = {}
+        for n in cands:
+            lms.replan(RewriteConfig(n_tensors=n if n < N else -1, lb=args.lb, ub=args.ub,
+                                     ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
+                                     swapin_fuse_distance=args.fuse_distance))
+            try:
+                info = lms.tune_windows(xs, ys)
+            except RuntimeError as e:
+                if not is_oom(e):
+                    raise
+                traceback.clear_frames(e.__traceback__)
+                info = {}
+            ms = [v for v in [info.get("base_ms"), info.get("trials", {}).get(info.get("moved"))] if v]
+            joint[n] = min(ms) if ms else None
+            log(f"[bench] joint n_tensors={n}: {joint[n]} ms ({info.get('moved')} moved)")
+            opt.zero_grad(set_to_none=True)
+            gc.collect()
+        fit = {n: v for n, v in joint.items() if v is not None}
+        if fit:
+            ok_ns = [min(fit, key=fit.get)]
     for n_use in sorted(set(ok_ns)):
         for tune in ((True, False) if args.tune_windows else (False,)):
             swap_ms = run_timed(n_use, tune)
@@ -704,6 +734,7 @@ def main():
                  "attempts": attempts, "capture_s": round(capture_s, 2),
                  "rewrite_s": round(plan.rewrite_seconds, 3), "bisect_s": round(bisect_s, 1),
                  "graph_nodes": len(lms.graph.nodes), "static_plan": lms.plan_note, "tune_windows": tuned,
+                 "joint_n_tensors_ms": joint,
                  "timed_host_grows": st1["n_host_grow"] - st0["n_host_grow"],
                  "timed_host_grow_ms": round(st1["host_grow_ms"] - st0["host_grow_ms"], 1),
                  "timed_page_moves": st1["n_reclaims"] - st0["n_reclaims"],
