@@ -504,17 +504,23 @@ def main():
     clk = None
 
     tuned = {}
+    prepared = None   # (cfg, plan, info) chosen by the joint search: timed as is
 
     def run_timed(n_use, tune=False):
         """Warm-up + exactly ``args.steps`` timed swapped steps; None if the budget is hit."""
-        nonlocal st0, clk, tuned
+        nonlocal st0, clk, tuned, prepared
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
                                  ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
                                  swapin_fuse_distance=args.fuse_distance))
         clocks = Clocks(local)
         tuned = {}
         try:
-            if tune:
+            if tune and prepared is not None:
+                lms.cfg = prepared[0]
+                lms._set_plan(prepared[1])
+                tuned = dict(prepared[2], reused=True)
+                prepared = None     # a retry (OOM) tunes afresh
+            elif tune:
                 tuned = lms.tune_windows(xs, ys)
                 log(f"[bench] tune_windows: {tuned}")
             for _ in range(args.warmup):
@@ -559,9 +565,8 @@ def main():
         # keep the fastest replayed step (each candidate's own untouched plan
         # included)
         n_min = min(ok_ns)
-        d = max(1, (N - n_min) // 4)
-        cands = sorted({n_min, min(N, n_min + d), min(N, n_min + 2 * d), N})
-        joint = {}
+        cands = sorted({min(N, n_min + (1 << k) - 1) for k in range(8)} | {N})
+        joint, joint_plan = {}, {}
         for n in cands:
             lms.replan(RewriteConfig(n_tensors=n if n < N else -1, lb=args.lb, ub=args.ub,
                                      ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
@@ -575,12 +580,15 @@ def main():
                 info = {}
             ms = [v for v in [info.get("base_ms"), info.get("trials", {}).get(info.get("moved"))] if v]
             joint[n] = min(ms) if ms else None
+            if ms:
+                joint_plan[n] = (lms.cfg, lms.plan, info)
             log(f"[bench] joint n_tensors={n}: {joint[n]} ms ({info.get('moved')} moved)")
             opt.zero_grad(set_to_none=True)
             gc.collect()
         fit = {n: v for n, v in joint.items() if v is not None}
         if fit:
             ok_ns = [min(fit, key=fit.get)]
+            prepared = joint_plan[ok_ns[0]]
     for n_use in sorted(set(ok_ns)):
         for tune in ((True, False) if args.tune_windows else (False,)):
             swap_ms = run_timed(n_use, tune)

@@ -811,8 +811,8 @@ class LMS:
         self._exec = SwapExecutor(self.ctx, plan, self.codec)
         self._drop_step_plan()
 
-    def _timed_replay(self, x, y):
-        """Re-record the current plan and time one replayed step (ms); None if the
+    def _timed_replay(self, x, y, steps: int = 2):
+        """Re-record the current plan and time ``steps`` replayed steps (ms per step); None if the
         placement does not fit at physical-release lifetimes or a step hits the budget."""
         self._drop_step_plan()
         try:
@@ -823,10 +823,11 @@ class LMS:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
-            self.step(x, y)
+            for _ in range(steps):
+                self.step(x, y)
             e1.record()
             torch.cuda.synchronize()
-            return e0.elapsed_time(e1)
+            return e0.elapsed_time(e1) / steps
         except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
             self.optimizer.zero_grad(set_to_none=True)
             torch.cuda.synchronize()
