@@ -450,6 +450,37 @@ def retarget(plan: SwapPlan, moves: dict) -> SwapPlan:
     return replace(plan, groups=groups, triggers=triggers)
 
 
+def plan_window_moves(live, node_clock: dict, issue: list, cands: dict, trigger: dict, limit: float) -> list:
+    """The model step of ``LMS.tune_windows`` (host only).
+
+    ``live``: bytes live per event of a recorded step (updated in place);
+    ``node_clock``: {node rank: event clock when it finished}; ``issue``:
+    [(clock, gid, bytes)] of the swap-ins; ``cands``: {gid: [candidate node
+    ranks]}; ``trigger``: {gid: current node rank}.  Swap-ins in issue order
+    each take the earliest candidate c2 < c1 with max(live[c2:c1]) + bytes <=
+    limit that does not pass the previous swap-in's trigger.  Returns
+    [(gid, c1, c2, bytes, rank)] in issue order."""
+    out, prev = [], -1
+    for c1, gid, nb in sorted(issue):
+        best = None
+        for r in cands.get(gid, ()):
+            c2 = node_clock.get(r)
+            if r == trigger.get(gid) or c2 is None or c2 >= c1 or c2 < prev:
+                continue
+            if best is not None and c2 >= best[1]:
+                continue
+            if live[c2:c1].max() + nb <= limit:
+                best = (r, c2)
+        if best is None:
+            prev = max(prev, c1)
+            continue
+        r, c2 = best
+        live[c2:c1] += nb
+        out.append((gid, c1, c2, nb, r))
+        prev = c2
+    return out
+
+
 class _SwapRef:
     """What autograd keeps instead of a swapped tensor."""
 
@@ -735,25 +766,8 @@ class LMS:
         start_peak = float(live.max()) if T else 0.0
         node_clock = probe["node_clock"]
         issue = sorted(((c, gid, nb) for gid, (c, nb) in probe["issue"].items() if gid in cands))
-        moves, prev, moved = {}, -1, []
-        for c1, gid, nb in issue:
-            best = None
-            for r in cands[gid]:
-                c2 = node_clock.get(r)
-                if r == self.plan.groups[gid].trigger or c2 is None or c2 >= c1 or c2 < prev:
-                    continue
-                if best is not None and c2 >= best[1]:
-                    continue
-                if live[c2:c1].max() + nb <= limit:
-                    best = (r, c2)
-            if best is None:
-                prev = max(prev, c1)
-                continue
-            r, c2 = best
-            live[c2:c1] += nb
-            moves[gid] = r
-            moved.append((gid, c1, c2, nb))
-            prev = c2
+        moved = plan_window_moves(live, node_clock, issue, cands,
+                                  {g.gid: g.trigger for g in self.plan.groups}, limit)
         # the live bytes bound the placement from below only: keep the longest
         # prefix of the moves (in issue order) whose recorded step, with those
         # destinations allocated at their new clocks, still places inside the
@@ -768,7 +782,7 @@ class LMS:
 
         def region_with(k):
             tk = list(t0)
-            for gid, c1, c2, nb in moved[:k]:
+            for gid, c1, c2, nb, _ in moved[:k]:
                 tk[item_at[c1]] = c2
             return rt.plan_solve(sizes, tk, t1)[1]
 
@@ -791,7 +805,7 @@ class LMS:
         trials = {}
         chosen = 0
         while keep > 0 and base_ms is not None:
-            self._set_plan(retarget(orig, {gid: moves[gid] for gid, *_ in moved[:keep]}))
+            self._set_plan(retarget(orig, {m[0]: m[4] for m in moved[:keep]}))
             ms = self._timed_replay(x, y)
             trials[keep] = ms
             if ms is not None and (ms < base_ms or not require_faster):
@@ -802,7 +816,7 @@ class LMS:
             self._set_plan(orig)
         self._drop_step_plan()
         return {"moved": chosen, "of": len(issue), "modelled": len(moved),
-                "moved_bytes": sum(nb for *_, nb in moved[:chosen]),
+                "moved_bytes": sum(m[3] for m in moved[:chosen]),
                 "base_ms": base_ms, "trials": trials, "peak_before": start_peak,
                 "limit": limit, "lower_bound": info["lower_bound_bytes"]}
 

@@ -123,3 +123,26 @@ def test_retarget_moves_triggers_and_keeps_issue_order():
         own = [gid for gid in near.triggers.get(r, []) if gid not in moves]
         assert gids[:len(own)] == own
     assert retarget(near, {}).triggers == near.triggers
+
+
+def test_plan_window_moves_respects_room_and_issue_order():
+    """The tune_windows model: each swap-in takes its earliest candidate whose
+    window keeps live + bytes under the limit, never before the previous
+    swap-in's trigger; accepted moves raise the live curve for later ones."""
+    import numpy as np
+    from paper_1807_02037_b200.torch_lms import plan_window_moves
+    live = np.full(100, 10.0)
+    live[20:30] = 18.0                      # a peak the first swap-in cannot span
+    node_clock = {1: 10, 2: 35, 3: 40, 4: 50, 5: 60, 6: 5}
+    issue = [(45, 0, 5.0), (70, 1, 4.0), (80, 2, 1.0)]
+    cands = {0: [1, 2], 1: [3, 6], 2: [4, 5]}
+    trig = {0: 9, 1: 9, 2: 5}
+    out = plan_window_moves(live, node_clock, issue, cands, trig, limit=20.0)
+    # gid 0: rank 1 (clock 10) spans the 18-byte peak (18 + 5 > 20) -> rank 2 (35)
+    # gid 1: rank 6 (clock 5) would pass gid 0's new trigger -> rank 3 (40)
+    # gid 2: rank 5 is its own trigger; rank 4 (50): live there is 10 + 4 + 1 <= 20
+    assert [(g, c2, r) for g, _, c2, _, r in out] == [(0, 35, 2), (1, 40, 3), (2, 50, 4)]
+    assert live[35:45].max() == 10 + 5 + 4 and live[60:70].max() == 10 + 4 + 1
+    # no room at all: nothing moves
+    live2 = np.full(100, 20.0)
+    assert plan_window_moves(live2, node_clock, issue, cands, trig, limit=20.0) == []
