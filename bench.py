@@ -70,9 +70,11 @@ def parse():
                     help="also time TFLMS (every candidate swapped) at B0 against the plain step at B0")
     ap.add_argument("--autotune", action="store_true",
                     help="pick lb empirically (LMS.autotune over 1,2,3,5,8) before the timed run")
-    ap.add_argument("--tune-windows", type=int, default=0,
+    ap.add_argument("--tune-windows", type=int, default=2,
                     help="memory-aware per-swap-in control ops (LMS.tune_windows) before the timed run; "
-                         "2 = also trade swapped-tensor count for prefetch room (tries a few n_tensors)")
+                         "2 = also trade swapped-tensor count for prefetch room (tries a few n_tensors); 0 = off")
+    ap.add_argument("--tune-budget-s", type=float, default=240.0,
+                    help="wall-clock budget of the joint search (candidates started after it are skipped)")
     ap.add_argument("--ddp", action="store_true",
                     help="wrap the model in DistributedDataParallel even at one rank (exercises the DP path)")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
@@ -222,6 +224,10 @@ def main():
     link = measure_host_link(torch, dev)
     gc.collect()
     use_dist = ws > 1 or args.ddp
+    if use_dist:
+        # tuning runs a rank-local, timing-dependent number of steps: under DDP
+        # every rank must step together, so replicas keep the rewrite's windows
+        args.tune_windows = 0
     if use_dist:
         import torch.distributed as dist
         for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511"), ("RANK", "0"), ("WORLD_SIZE", "1")):
@@ -565,9 +571,17 @@ def main():
         # keep the fastest replayed step (each candidate's own untouched plan
         # included)
         n_min = min(ok_ns)
-        cands = sorted({min(N, n_min + (1 << k) - 1) for k in range(8)} | {N})
+        grid = sorted({min(N, n_min + (1 << k) - 1) for k in range(8)} | {N})
+        # the fewest that fit first (the untuned baseline), then from the
+        # largest down: at a deep oversubscription only near-full swap sets
+        # leave room; at a shallow one each candidate's steps are cheap
+        cands = [n_min] + sorted((n for n in grid if n != n_min), reverse=True)
         joint, joint_plan = {}, {}
+        t_joint = time.perf_counter()
         for n in cands:
+            if time.perf_counter() - t_joint > args.tune_budget_s:
+                log(f"[bench] joint search budget spent; skipping n_tensors={n}")
+                break
             lms.replan(RewriteConfig(n_tensors=n if n < N else -1, lb=args.lb, ub=args.ub,
                                      ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
                                      swapin_fuse_distance=args.fuse_distance))
@@ -724,7 +738,8 @@ def main():
                    "parallelism": f"dp{ws}" if use_dist else "single",
                    "l2": "inputs (>=450 MB/step) exceed L2; no flush",
                    "rewrite": {"lb": args.lb, "ub": args.ub, "ctrld_strategy": args.strategy,
-                               "fuse_swapins": args.fuse_swapins, "n_tensors": plan.report.tensors_swapped},
+                               "fuse_swapins": args.fuse_swapins, "n_tensors": plan.report.tensors_swapped,
+                               "tune_windows": args.tune_windows, "swap_ins_moved": (tuned or {}).get("moved", 0)},
                    "codec": args.codec},
         "no_swap": {"batch": b0, "img_s": round(noswap_ips, 2) if noswap_ips else None,
                     "ms_per_step": round(noswap_ms / steps, 3) if noswap_ms else None},
