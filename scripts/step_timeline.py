@@ -55,6 +55,8 @@ def main():
     ap.add_argument("--n-tensors", type=int, default=-1)
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--no-plan", action="store_true")
+    ap.add_argument("--fuse-distance", type=int, default=1)
+    ap.add_argument("--tune", action="store_true", help="LMS.tune_windows before the traced steps")
     args = ap.parse_args()
 
     import torch
@@ -74,7 +76,7 @@ def main():
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
     lf = torch.nn.functional.cross_entropy
     cfg = RewriteConfig(lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy, fuse_swapins=True,
-                        swapin_fuse_distance=1, n_tensors=args.n_tensors)
+                        swapin_fuse_distance=args.fuse_distance, n_tensors=args.n_tensors)
     lms = LMS(model, lf, opt, cfg, ctx, codec=args.codec, min_swap_bytes=(256 << 10) // 4,
               static_plan=not args.no_plan)
     xc = torch.randn(4, 3, 224, 224, device=dev)
@@ -85,6 +87,7 @@ def main():
     y = torch.randint(0, 1000, (args.batch,), device=dev)
     s = torch.cuda.current_stream()
     marks = {}
+    tuned = lms.tune_windows(x, y) if args.tune else None
 
     run = lms._exec.run
 
@@ -123,7 +126,7 @@ def main():
     both = d2h + h2d
     st = ctx.stats()
     res = {
-        "batch": args.batch, "codec": args.codec, "lb": args.lb, "plan": lms.plan.summary(),
+        "batch": args.batch, "codec": args.codec, "lb": args.lb, "plan": lms.plan.summary(), "tune_windows": tuned,
         "step_ms": te - t0, "fwd_ms": tf - t0, "bwd_opt_ms": te - tf,
         "fwd": {"d2h_busy": union(d2h, t0, tf), "h2d_busy": union(h2d, t0, tf), "any_busy": union(both, t0, tf)},
         "bwd": {"d2h_busy": union(d2h, tf, te), "h2d_busy": union(h2d, tf, te), "any_busy": union(both, tf, te)},
