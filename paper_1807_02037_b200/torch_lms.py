@@ -811,7 +811,7 @@ class LMS:
             if ms is not None and (ms < base_ms or not require_faster):
                 chosen = keep
                 break
-            keep //= 2
+            keep = keep * 2 // 3
         if not chosen:
             self._set_plan(orig)
         self._drop_step_plan()
