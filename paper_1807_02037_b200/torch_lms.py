@@ -721,7 +721,7 @@ class LMS:
         trigger (the H2D channel stays in consumer order).  The longest prefix
         of those moves whose placement the pool's solver fits is then tried
         for real: re-targeted (``retarget``), re-recorded and one replayed step
-        timed against the untouched plan; the set is halved until a replay
+        timed against the untouched plan; the set shrinks by a third until a replay
         fits and is faster, or dropped.  The model parameters move by the
         probe and trial steps (like ``autotune``).  Returns a summary dict;
         ``{}`` changes nothing (no room, or no static plan to measure)."""
