@@ -510,11 +510,12 @@ def main():
     clk = None
 
     tuned = {}
+    extra_warmup = 0
     prepared = None   # (cfg, plan, info) chosen by the joint search: timed as is
 
     def run_timed(n_use, tune=False):
         """Warm-up + exactly ``args.steps`` timed swapped steps; None if the budget is hit."""
-        nonlocal st0, clk, tuned, prepared
+        nonlocal st0, clk, tuned, prepared, extra_warmup
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
                                  ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
                                  swapin_fuse_distance=args.fuse_distance))
@@ -531,6 +532,18 @@ def main():
                 log(f"[bench] tune_windows: {tuned}")
             for _ in range(args.warmup):
                 lms.step(xs, ys)
+            # untimed settling: the pool may still move pages for the step's
+            # unplanned allocations after a (re)plan (tuning trials leave it
+            # fragmented); up to 3 more warm-up steps until one moves none
+            extra_warmup = 0
+            torch.cuda.synchronize(dev)
+            while extra_warmup < 3:
+                r0 = ctx.stats()["n_reclaims"]
+                lms.step(xs, ys)
+                torch.cuda.synchronize(dev)
+                extra_warmup += 1
+                if ctx.stats()["n_reclaims"] == r0:
+                    break
             torch.cuda.synchronize(dev)
             ctx.trace_clear()
             ctx.reset_peaks()
@@ -756,7 +769,7 @@ def main():
                  "device_peak_bytes": st1["device_peak"], "host_peak_bytes": st1["host_peak"],
                  "attempts": attempts, "capture_s": round(capture_s, 2),
                  "rewrite_s": round(plan.rewrite_seconds, 3), "bisect_s": round(bisect_s, 1),
-                 "graph_nodes": len(lms.graph.nodes), "static_plan": lms.plan_note, "tune_windows": tuned,
+                 "graph_nodes": len(lms.graph.nodes), "static_plan": lms.plan_note, "tune_windows": tuned, "settling_warmup_steps": extra_warmup,
                  "joint_n_tensors_ms": joint,
                  "timed_host_grows": st1["n_host_grow"] - st0["n_host_grow"],
                  "timed_host_grow_ms": round(st1["host_grow_ms"] - st0["host_grow_ms"], 1),
