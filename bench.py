@@ -686,12 +686,13 @@ def main():
     cpu = None
     if rank == 0 and args.cpu_baseline:
         from oracle.cpu_step import resnet_cpu_step_rate
-        ips, cores, detail = resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=2, warmup=1,
+        ips, cores, detail = resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=5, warmup=2,
                                                   budget_s=20, image=cpu_size(args))
         cpu = {"value": round(ips, 3), "unit": unit_name(args), "cores": cores, "kind": "port",
                "sample": f"{args.arch} fp32 train step on host cores, batch {detail['batch']} at "
                          f"{cpu_size(args)} px/voxels per edge, "
-                         f"{detail['steps']} steps (swaps = identities, interp.py:168-170)"}
+                         f"{detail['steps']} steps (swaps = identities, interp.py:168-170)",
+               "c1_interpret": c1_interpret_baseline()}
 
     kernels = st1["kernel_launches"] - st0["kernel_launches"]
     # per transfer path: wire bytes over the summed spans of its transfers
@@ -850,22 +851,40 @@ def cpu_size(args) -> int:
     return 96 if args.arch == "unet3d" else (args.size or 224)
 
 
+def c1_interpret_baseline(layers: int = 8, n: int = 1024, repeats: int = 3) -> dict:
+    """the reference CPU executor (``interpret``, fp64 numpy on all
+    host cores) on configs[0]'s feed-forward chain, with and without the lb=1/ub=3
+    rewrite, best of ``repeats``."""
+    from oracle.interp_oracle import interpret as oracle_interpret
+    from paper_1807_02037_b200 import RewriteConfig, rewrite
+    from paper_1807_02037_b200.workloads import ffchain, ffchain_inputs
+
+    g = ffchain(layers, n)
+    inputs = ffchain_inputs(g, n, seed=0)
+    g2, _ = rewrite(g, RewriteConfig(lb=1, ub=3))
+    out = {"workload": f"ffchain L={layers} N={n} fp64 (interp.py:58-163)",
+           "threads": len(os.sched_getaffinity(0))}
+    for label, graph in (("no_swap_ms", g), ("swap_ms", g2)):
+        best = math.inf
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            oracle_interpret(graph, inputs)
+            best = min(best, time.perf_counter() - t0)
+        out[label] = round(best * 1e3, 1)
+    return out
+
+
 def run_reference(args, ws, rank):
     if ws > 1 and rank != 0:
         return
     from oracle.cpu_step import resnet_cpu_step_rate
-    rates = []
-    for _ in range(max(1, args.warmup)):
-        resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=1, warmup=0, budget_s=60,
-                             image=cpu_size(args))
-    t0 = time.perf_counter()
-    cores = None
-    for _ in range(args.steps):
-        ips, cores, _ = resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=1, warmup=0, budget_s=60,
-                                             image=cpu_size(args))
-        rates.append(ips)
-    dt = time.perf_counter() - t0
-    value = cpu_batch(args) * args.steps / dt
+    # the model, optimizer and batch are built once; warm-up steps run untimed
+    # and only the timed steps count (bounded: the whole run stays within minutes)
+    value, cores, detail = resnet_cpu_step_rate(args.arch, batch=cpu_batch(args), steps=args.steps,
+                                                warmup=max(1, args.warmup), budget_s=180,
+                                                image=cpu_size(args))
+    dt = detail["seconds"]
+    args.steps = detail["steps"]
     out = {
         "impl": "reference",
         "metric": metric_name(args),

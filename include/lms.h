@@ -224,6 +224,16 @@ int lms_zvc_decode(lms_ctx* ctx, const void* enc, size_t nwords, void* dst, void
 /* bytes used by an encoded stream whose header is host-readable */
 int lms_zvc_encoded_size(const void* enc_host, size_t* out);
 
+/* ---- measured simulation (replaces sim.py:139-476's modelled op) ----------- */
+/* One graph op of a replayed schedule (the GPU-measured `simulate`): checks
+ * each input against the word pattern of its origin tensor tag (mismatching
+ * words are added to *errors, a device counter), fills each output with its
+ * own tag's pattern, and lasts at least spin_ns (the node's cost_hint,
+ * sim.py:350-352).  Ops with more than 8 inputs/outputs take several launches. */
+int lms_sim_op(lms_ctx* ctx, void* const* outs, const uint64_t* out_bytes, const uint32_t* out_tags, int n_out,
+               const void* const* ins, const uint64_t* in_bytes, const uint32_t* in_tags, int n_in,
+               uint64_t spin_ns, uint32_t* errors, void* stream);
+
 /* ---- stats / trace -------------------------------------------------------- */
 /* sizes of live device blocks, largest first (diagnostics); *n = total count */
 int lms_live_blocks(lms_ctx* ctx, uint64_t* sizes, size_t cap, size_t* n);

@@ -611,6 +611,72 @@ __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict_
   }
 }
 
+// -------------------------------------------------------------------------
+// Replay payload of one graph op (lms_sim_op, the measured `simulate`): each
+// input is checked word by word against the pattern its origin tensor was
+// written with (a swap chain must deliver exactly those bytes), each output
+// is filled with its own pattern, and the op lasts at least `spin_ns` (the
+// node's cost_hint).  Pure HBM streaming: uint4 accesses where aligned.
+
+constexpr int kSimMaxArgs = 8;
+
+struct SimArgs {
+  const void* in[kSimMaxArgs];
+  void* out[kSimMaxArgs];
+  uint64_t in_bytes[kSimMaxArgs], out_bytes[kSimMaxArgs];
+  uint32_t in_tag[kSimMaxArgs], out_tag[kSimMaxArgs];
+  int n_in, n_out;
+};
+
+__device__ __forceinline__ uint32_t sim_word(uint32_t tag, uint64_t i) {
+  uint32_t x = tag * 0x9E3779B1u ^ uint32_t(i) * 0x85EBCA77u ^ uint32_t(i >> 32) * 0xC2B2AE3Du;
+  x ^= x >> 15;
+  return x * 0x2C1B3C6Du;
+}
+
+__global__ void __launch_bounds__(256) sim_op_kernel(SimArgs a, uint64_t spin_ns, uint32_t* __restrict__ errors) {
+  uint64_t t_start = 0;
+  if (spin_ns && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nth = uint64_t(gridDim.x) * blockDim.x;
+  uint32_t bad = 0;
+  for (int k = 0; k < a.n_in; ++k) {
+    const uint32_t* p = static_cast<const uint32_t*>(a.in[k]);
+    const uint64_t nw = a.in_bytes[k] / 4;
+    const uint32_t tag = a.in_tag[k];
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const uint64_t n4 = nw / 4;
+      for (uint64_t i = tid; i < n4; i += nth) {
+        const uint4 v = ld_stream(reinterpret_cast<const uint4*>(p) + i);
+        bad += (v.x != sim_word(tag, 4 * i)) + (v.y != sim_word(tag, 4 * i + 1)) +
+               (v.z != sim_word(tag, 4 * i + 2)) + (v.w != sim_word(tag, 4 * i + 3));
+      }
+      for (uint64_t i = n4 * 4 + tid; i < nw; i += nth) bad += p[i] != sim_word(tag, i);
+    } else {
+      for (uint64_t i = tid; i < nw; i += nth) bad += p[i] != sim_word(tag, i);
+    }
+  }
+  for (int k = 0; k < a.n_out; ++k) {
+    uint32_t* p = static_cast<uint32_t*>(a.out[k]);
+    const uint64_t nw = a.out_bytes[k] / 4;
+    const uint32_t tag = a.out_tag[k];
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const uint64_t n4 = nw / 4;
+      for (uint64_t i = tid; i < n4; i += nth)
+        st_stream(reinterpret_cast<uint4*>(p) + i, make_uint4(sim_word(tag, 4 * i), sim_word(tag, 4 * i + 1),
+                                                              sim_word(tag, 4 * i + 2), sim_word(tag, 4 * i + 3)));
+      for (uint64_t i = n4 * 4 + tid; i < nw; i += nth) p[i] = sim_word(tag, i);
+    } else {
+      for (uint64_t i = tid; i < nw; i += nth) p[i] = sim_word(tag, i);
+    }
+  }
+  if (bad) atomicAdd(errors, bad);
+  if (spin_ns && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t now = t_start;
+    while (now - t_start < spin_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  }
+}
+
 }  // namespace lms
 
 // -------------------------------------------------------------------------

@@ -1824,6 +1824,42 @@ int lms_zvc_decode(lms_ctx* c, const void* enc, size_t nwords, void* dst, void* 
                            static_cast<cudaStream_t>(stream), is_host_ptr(enc));
 }
 
+int lms_sim_op(lms_ctx* c, void* const* outs, const uint64_t* out_bytes, const uint32_t* out_tags, int n_out,
+               const void* const* ins, const uint64_t* in_bytes, const uint32_t* in_tags, int n_in,
+               uint64_t spin_ns, uint32_t* errors, void* stream) {
+  if (!c || !errors || n_in < 0 || n_out < 0 || (n_in && (!ins || !in_bytes || !in_tags)) ||
+      (n_out && (!outs || !out_bytes || !out_tags)))
+    return fail(LMS_E_INVALID, "lms_sim_op: null argument");
+  uint64_t total = 0;
+  for (int k = 0; k < n_in; ++k) total += in_bytes[k];
+  for (int k = 0; k < n_out; ++k) total += out_bytes[k];
+  // ops with more operands than one launch carries run as several launches
+  int i0 = 0, o0 = 0;
+  do {
+    SimArgs a{};
+    a.n_in = std::min(n_in - i0, kSimMaxArgs);
+    a.n_out = std::min(n_out - o0, kSimMaxArgs);
+    for (int k = 0; k < a.n_in; ++k) {
+      a.in[k] = ins[i0 + k];
+      a.in_bytes[k] = in_bytes[i0 + k];
+      a.in_tag[k] = in_tags[i0 + k];
+    }
+    for (int k = 0; k < a.n_out; ++k) {
+      a.out[k] = outs[o0 + k];
+      a.out_bytes[k] = out_bytes[o0 + k];
+      a.out_tag[k] = out_tags[o0 + k];
+    }
+    i0 += a.n_in;
+    o0 += a.n_out;
+    const bool last = i0 >= n_in && o0 >= n_out;
+    const int grid = sm_grid(c, int64_t(total / 16 + 1), 256 * 4);
+    sim_op_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, last ? spin_ns : 0, errors);
+    c->st.kernel_launches++;
+    CK(cudaGetLastError());
+  } while (i0 < n_in || o0 < n_out);
+  return LMS_OK;
+}
+
 int lms_zvc_encoded_size(const void* enc_host, size_t* out) {
   if (!enc_host || !out) return fail(LMS_E_INVALID, "null argument");
   const ZvcHeader* h = static_cast<const ZvcHeader*>(enc_host);

@@ -22,8 +22,10 @@ class DeadlockError(RuntimeError):
 
 @dataclass(frozen=True)
 class SimConfig:
-    """Capacity and link model (sim.py:47-71); the executor reads
-    ``device_capacity_bytes`` as its enforced pool budget."""
+    """Capacity and link model (sim.py:47-71).  The measured ``simulate``
+    (simulate.py) enforces ``device_capacity_bytes`` as its pool budget and maps
+    ``overlap_transfers`` onto separate or shared copy streams; the bandwidths
+    are not modelled there (the host link is real)."""
 
     device_capacity_bytes: int = 16 * 2**30
     host_to_device_bandwidth: float = float(80 * 2**30)

@@ -121,6 +121,9 @@ def lib():
         "lms_trace_clear": ([vp], i), "lms_synchronize": ([vp], i),
         "lms_trim": ([vp, sz, ctypes.POINTER(sz)], i),
         "lms_live_blocks": ([vp, ctypes.POINTER(ctypes.c_uint64), sz, ctypes.POINTER(sz)], i),
+        "lms_sim_op": ([vp, pp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), i,
+                        pp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), i,
+                        ctypes.c_uint64, vp, vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -215,6 +218,12 @@ class Context:
         return (torch.cuda.ExternalStream(a.value, device=dev),
                 torch.cuda.ExternalStream(b.value, device=dev))
 
+    def _d2h_stream(self):
+        s = getattr(self, "_d2h_ext", None)
+        if s is None:
+            s = self._d2h_ext = self.streams()[0]
+        return s
+
     def trim(self, min_zombies: int = 1) -> int:
         """Unmap stale VA aliases left by page moves once there are at least
         ``min_zombies`` (blocks until the device drains)."""
@@ -269,6 +278,13 @@ class Context:
         _check(lib().lms_swap_out(self.ptr, t.data_ptr(), _i64(sizes), _i64(strides), t.dim(),
                                   t.element_size(), _stream_ptr(stream), code, ctypes.byref(h)),
                "lms_swap_out")
+        if _installed is not self and t.numel():
+            # liblms holds the source block until the D2H lands only when its own
+            # pool owns it (lms.h: lms_swap_out).  Any other allocator (PyTorch's
+            # caching allocator when this context is not installed) must not hand
+            # the block to the compute stream while the D2H channel still reads it:
+            # recordStream defers its reuse past the work now queued on that channel.
+            t.record_stream(self._d2h_stream())
         hid = ctypes.c_int64()
         logical = ctypes.c_uint64()
         _check(lib().lms_handle_info(h.value, ctypes.byref(hid), ctypes.byref(logical), None, None),
@@ -360,6 +376,36 @@ class Context:
     def zvc_decode(self, enc, dst, stream=None):
         _check(lib().lms_zvc_decode(self.ptr, enc.data_ptr(), dst.numel() * dst.element_size() // 4,
                                     dst.data_ptr(), _stream_ptr(stream)), "lms_zvc_decode")
+
+    def sim_op(self, outs, ins, errors: int, spin_ns: int = 0, stream=None):
+        """One replayed graph op (``lms_sim_op``): ``outs``/``ins`` are lists of
+        (device pointer, bytes, pattern tag)."""
+        no, ni = len(outs), len(ins)
+        P = ctypes.c_void_p * max(1, no)
+        Q = ctypes.c_void_p * max(1, ni)
+        U64o, U64i = ctypes.c_uint64 * max(1, no), ctypes.c_uint64 * max(1, ni)
+        U32o, U32i = ctypes.c_uint32 * max(1, no), ctypes.c_uint32 * max(1, ni)
+        _check(lib().lms_sim_op(self.ptr, P(*[o[0] for o in outs]), U64o(*[o[1] for o in outs]),
+                                U32o(*[o[2] & 0xFFFFFFFF for o in outs]), no,
+                                Q(*[x[0] for x in ins]), U64i(*[x[1] for x in ins]),
+                                U32i(*[x[2] & 0xFFFFFFFF for x in ins]), ni, int(spin_ns), errors,
+                                _stream_ptr(stream)), "lms_sim_op")
+
+    def swap_out_raw(self, ptr: int, nbytes: int, codec: str | int = "ce", stream=None) -> SwapHandle:
+        """Swap out ``nbytes`` of raw device memory (a 1-D byte view)."""
+        import torch
+        code = CODECS[codec] if isinstance(codec, str) else int(codec)
+        h = ctypes.c_void_p()
+        _check(lib().lms_swap_out(self.ptr, ptr, _i64([nbytes]), _i64([1]), 1, 1, _stream_ptr(stream), code,
+                                  ctypes.byref(h)), "lms_swap_out")
+        hid = ctypes.c_int64()
+        _check(lib().lms_handle_info(h.value, ctypes.byref(hid), None, None, None), "lms_handle_info")
+        return SwapHandle(h.value, hid.value, (nbytes,), torch.uint8, nbytes, (1,), nbytes)
+
+    def swap_in_raw(self, h: SwapHandle, dst_ptr: int, trigger_stream=None):
+        if h.released:
+            raise RuntimeError("swap_in of a released handle")
+        _check(lib().lms_swap_in(self.ptr, h.ptr, dst_ptr, None, _stream_ptr(trigger_stream)), "lms_swap_in")
 
     # -- reporting ----------------------------------------------------------------
     def stats(self) -> dict:

@@ -239,8 +239,62 @@ def write(name, obj):
     print(f"wrote {path} ({os.path.getsize(path)} bytes)")
 
 
+def make_api_cases():
+    """The public pass functions on their own (insert_swap_pair, attach_control,
+    free_step_oracle) and the reference's import surface (__init__.py:60-115)."""
+    graphs = [(f"fixture:{n}", getattr(F, n)()) for n in
+              ("expression_graph", "hot_fanout_graph", "three_op_chain", "two_layer_training_graph",
+               "clustered_consumers_graph", "training_expression_graph")]
+    graphs += [("gen:chain(6)", RG.chain(6)), ("gen:unet(3)", RG.unet(3)), ("gen:resnet_like(3)", RG.resnet_like(3))]
+    graphs += [(f"graphgen:{s}", graphgen.training_graph(s)) for s in range(12)]
+    inserts, attaches, frees, bares = [], [], [], {}
+    for name, g in graphs:
+        order = R.topo_order(g)
+        cands = R.select_candidates(g, order, R.RewriteConfig(swap_branches=True, branch_threshold=0))
+        probes = [e for e, _ in cands][:6]
+        probes.append(R.EdgeRec(g.max_node_id() + 5, g.max_node_id() + 6, R.EdgeAction.READ, 0))
+        probes += [e for e in g.edges if e.action is not R.EdgeAction.READ][:1]
+        for e in probes:
+            entry = {"edge": [e.src, e.dst, e.action.value, e.tensor]}
+            try:
+                out, so, si = R.insert_swap_pair(g, e)
+                entry.update(sha256=sha(R.dumps(out)), so=so, si=si)
+            except Exception as exc:
+                entry["error"] = f"{type(exc).__name__}: {exc}"
+            inserts.append(dict(entry, graph=name))
+        try:
+            out, _ = R.rewrite(g, R.RewriteConfig(n_tensors=2))
+        except R.RewriteError:
+            out = g   # no phase tags: attach_control still applies to the bare graph
+        # drop the rewrite's own control edges so attach_control sees bare swap-ins
+        bare = R.CompGraph(out.nodes, tuple(e for e in out.edges if e.action is not R.EdgeAction.CONTROL),
+                           out.tensors)
+        bares[name + ":bare"] = R.graph_to_dict(bare)
+        sis = [n.id for n in bare.nodes if n.kind is R.NodeKind.SWAP_IN][:2]
+        ids = sorted(bare.node_by_id)
+        for si in sis + [ids[0]]:
+            for ctrl in ids[:: max(1, len(ids) // 9)] + [10 ** 6]:
+                entry = {"graph": name + ":bare", "ctrl": ctrl, "swap_in": si}
+                try:
+                    entry["sha256"] = sha(R.dumps(R.attach_control(bare, ctrl, si)))
+                except Exception as exc:
+                    entry["error"] = f"{type(exc).__name__}: {exc}"
+                attaches.append(entry)
+        for vg in (g, out):
+            vo = R.topo_order(vg)
+            frees.append({"graph": R.graph_to_dict(vg), "order": {str(k): v for k, v in vo.items()},
+                          "free_steps": {str(t.id): R.free_step_oracle(vg, vo, t.id) for t in vg.tensors}})
+    graph_dicts = {name: R.graph_to_dict(g) for name, g in graphs}
+    graph_dicts.update(bares)
+    return {"reference_all": sorted(R.__all__), "graphs": graph_dicts, "insert_swap_pair": inserts,
+            "attach_control": attaches, "free_step_oracle": frees}
+
+
 if __name__ == "__main__":
-    write("rewrite_cases.json.gz", make_rewrite_cases())
-    write("ctrl_queries.json.gz", make_ctrl_queries())
-    write("interp_cases.json.gz", make_interp_cases())
-    write("sim_cases.json.gz", make_sim_cases())
+    only = sys.argv[1:]
+    makers = {"rewrite_cases.json.gz": make_rewrite_cases, "ctrl_queries.json.gz": make_ctrl_queries,
+              "interp_cases.json.gz": make_interp_cases, "sim_cases.json.gz": make_sim_cases,
+              "api_cases.json.gz": make_api_cases}
+    for fname, fn in makers.items():
+        if not only or fname in only:
+            write(fname, fn())
