@@ -36,6 +36,8 @@ import time
 from dataclasses import dataclass, field
 
 import torch
+from torch.overrides import TorchFunctionMode
+from torch.utils._pytree import tree_flatten
 
 from .graph import (
     CompGraph,
@@ -100,9 +102,15 @@ class SwapGroup:
     gid: int
     saved: int                  # index into plan.saved
     packs: list                 # pack indices this group serves
-    trigger: int | None         # node rank of the control op's backward node; None = eager
-    trigger_kind: str           # "backward" | "forward->bwd-start" | "eager"
+    trigger: int | None         # node rank of the control op's node; None = eager
+    trigger_kind: str           # "backward" | "forward->bwd-start" | "eager" | "forward"
     node: int = -1              # the swap-in node's id in the rewritten graph
+    # forward-side swap-ins (swap_branches: fwd->fwd edges, rewriter.py:231)
+    fwd_consumers: tuple = ()   # node ranks of the forward ops reading the swapped-in tensor
+    tensor: int = -1            # the captured graph's tensor id
+    producer_rank: int = -1     # node rank of the tensor's producer
+    release_rank: int = -1      # last forward op still reading the device copy
+    nbytes: int = 0
 
 
 @dataclass
@@ -124,6 +132,8 @@ class SwapPlan:
     saved_bytes_per_step: int
     capture_batch: int
     rewrite_seconds: float
+    fwd_groups: list = field(default_factory=list)      # forward-side swap-in groups
+    fwd_triggers: dict = field(default_factory=dict)    # forward node rank -> [group ids]
 
     def summary(self) -> dict:
         return {
@@ -132,6 +142,7 @@ class SwapPlan:
             "swap_ins": len(self.groups),
             "control_edges": self.report.control_edges_added,
             "eager_swap_ins": len(self.eager_groups),
+            "forward_swap_ins": len(self.fwd_groups),
             "bwd_start_swap_ins": len(self.bwd_start_groups),
             "swapped_bytes_capture": self.swapped_bytes_per_step,
             "saved_bytes_capture": self.saved_bytes_per_step,
@@ -182,6 +193,28 @@ class _Capture:
         return t
 
 
+class _OutputBytes(TorchFunctionMode):
+    """Capture: bytes of every autograd node's forward output, so forward->forward
+    edges (the paper's branch tensors, e.g. U-Net skips) carry real sizes."""
+
+    def __init__(self):
+        super().__init__()
+        self.nbytes = {}
+        self.first = None
+
+    def __torch_function__(self, func, types, args=(), kwargs=None):
+        out = func(*args, **(kwargs or {}))
+        for t in tree_flatten(out)[0]:
+            if isinstance(t, torch.Tensor) and t.grad_fn is not None:
+                gf = t.grad_fn
+                if self.first is None:
+                    self.first = gf
+                nb = t.numel() * t.element_size()
+                if nb > self.nbytes.get(gf, -1):
+                    self.nbytes[gf] = nb
+        return out
+
+
 def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
     """Trace one step — ``forward_fn()`` returns the loss, backward runs here — into a CompGraph.
 
@@ -195,7 +228,8 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
     """
     keep_ptrs = {t.data_ptr() for t in persistent if t is not None and t.numel()}
     cap = _Capture()
-    with torch.autograd.graph.saved_tensors_hooks(cap.pack, cap.unpack):
+    sizes = _OutputBytes()
+    with torch.autograd.graph.saved_tensors_hooks(cap.pack, cap.unpack), sizes:
         loss = forward_fn()
     root = loss.grad_fn
     nodes = _walk(root)
@@ -316,6 +350,12 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
             seen_edge.add(e)
             gedges.append(e)
 
+    # forward outputs nobody saved: their fwd->fwd edges carry the output's bytes
+    for n in ops:
+        tid = main_out[n]
+        if gtensors[tid].size_bytes == 0 and sizes.nbytes.get(n, 0) > 0:
+            gtensors[tid] = TensorSpec(tid, F[n], sizes.nbytes[n])
+
     for a, users in acc_grad.items():
         v, vt = var_of_acc[a]
         uid = len(gnodes)
@@ -335,6 +375,10 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
         "F": {F[n]: rank[n] for n in ops},
         "B": {B[n]: rank[n] for n in ops},
         "consumer_rank": {k: rank.get(c) for k, c in cap.consumer.items()},
+        "min_swap_bytes": min_swap_bytes,
+        # forward-side swaps find op outputs by their node's rank counted from
+        # the first node the forward creates; that must be rank 0 here
+        "fwd_ranks_ok": sizes.first is not None and rank.get(sizes.first) == 0,
     }
     return g, meta
 
@@ -375,6 +419,7 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
     pack_group = {}
     triggers: dict[int, list] = {}
     bwd_start, eager = [], []
+    fwd_groups, fwd_triggers = [], {}
     ctrl_of = {e.dst: e.src for e in out.edges if e.action is EdgeAction.CONTROL}
     biggest = max((s.nbytes for s in saved_info if s.swapped), default=0)
     for n in out.nodes:
@@ -383,10 +428,24 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
         src = next(e for e in out.in_edges(n.id) if e.action is EdgeAction.READ)
         so = src.src
         orig = next(e for e in out.in_edges(so) if e.action is EdgeAction.READ).tensor
-        si = tid_to_saved[orig]
-        consumers = {B[e.dst] for e in out.out_edges(n.id) if e.action is EdgeAction.READ}
-        packs = [k for k in meta["saved"][si].packs if meta["consumer_rank"].get(k) in consumers]
+        si = tid_to_saved.get(orig)
+        dsts = [e.dst for e in out.out_edges(n.id) if e.action is EdgeAction.READ]
+        bwd_cons = {B[d] for d in dsts if d in B}
+        fwd_cons = sorted(F[d] for d in dsts if d in F)
         c = ctrl_of.get(n.id)
+        if fwd_cons:
+            # a branch swap (fwd->fwd, rewriter.py:231): the forward pass itself
+            # frees the device copy and restores it before the consumer
+            grp = _forward_group(out, meta, n.id, orig, si, fwd_cons, c, len(groups) + len(fwd_groups))
+            if grp is not None:
+                fwd_groups.append(grp)
+                if grp.trigger_kind == "forward":
+                    fwd_triggers.setdefault(grp.trigger, []).append(grp.gid)
+            if not bwd_cons:
+                continue
+        if si is None:
+            continue
+        packs = [k for k in meta["saved"][si].packs if meta["consumer_rank"].get(k) in bwd_cons]
         if far_ctrl and meta["saved"][si].nbytes < far_max_fraction * biggest and n.id in far_ctrl:
             c = far_ctrl[n.id]
         if c is None:
@@ -395,7 +454,7 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
             kind, trig = "backward", B[c]
         else:
             kind, trig = "forward->bwd-start", None
-        grp = SwapGroup(len(groups), si, packs, trig, kind, n.id)
+        grp = SwapGroup(len(groups) + len(fwd_groups), si, packs, trig, kind, n.id)
         groups.append(grp)
         for k in packs:
             pack_group[k] = grp.gid
@@ -405,6 +464,10 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
             eager.append(grp.gid)
         else:
             bwd_start.append(grp.gid)
+    # group ids index plan.groups: forward groups take their slots after renumbering
+    allg = sorted(groups + fwd_groups, key=lambda g: g.gid)
+    assert [g.gid for g in allg] == list(range(len(allg)))
+    groups = allg
     # packs of a swapped tensor whose consumer edge was not rewritten keep the tensor
     pack_is_swapped = [k in pack_group for k in range(meta["n_packs"])]
     swapped_bytes = sum(s.nbytes for s in saved_info if s.swapped)
@@ -415,9 +478,31 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
         bwd_start_groups=bwd_start, eager_groups=eager,
         swapped_bytes_per_step=swapped_bytes,
         saved_bytes_per_step=sum(s.nbytes for s in saved_info),
-        capture_batch=capture_batch, rewrite_seconds=dt)
+        capture_batch=capture_batch, rewrite_seconds=dt,
+        fwd_groups=[g.gid for g in fwd_groups], fwd_triggers=fwd_triggers)
     _ = F
     return plan
+
+
+def _forward_group(out: CompGraph, meta: dict, node: int, orig: int, si, fwd_cons, ctrl, gid):
+    """The forward side of one branch swap-in node, or None when it stays an
+    identity on the device (too small, or its ranks cannot be tracked)."""
+    F = meta["F"]
+    t = out.tensor_by_id[orig]
+    if not meta.get("fwd_ranks_ok") or t.producer not in F or t.size_bytes < meta.get("min_swap_bytes", 0):
+        return None
+    prod = F[t.producer]
+    # the device copy must stay until the forward readers the rewrite left in place have run
+    keep = [F[e.dst] for e in out.consumer_edges(orig) if e.action is EdgeAction.READ and e.dst in F]
+    release = max([prod] + keep)
+    if ctrl is None:
+        kind, trig = "eager", None
+    elif ctrl in F:
+        kind, trig = "forward", F[ctrl]
+    else:
+        return None
+    return SwapGroup(gid, -1 if si is None else si, [], trig, kind, node, fwd_consumers=tuple(fwd_cons),
+                     tensor=orig, producer_rank=prod, release_rank=release, nbytes=t.size_bytes)
 
 
 def _issuer(issue, gids):
@@ -479,6 +564,120 @@ def plan_window_moves(live, node_clock: dict, issue: list, cands: dict, trigger:
         out.append((gid, c1, c2, nb, r))
         prev = c2
     return out
+
+
+class _ForwardSwaps(TorchFunctionMode):
+    """Forward-side interception for branch swaps (swap_branches, rewriter.py:231).
+
+    Saved-tensor hooks only see tensors autograd keeps for backward; a U-Net
+    skip tensor is also held by the model's own Python references until its
+    forward consumer (the concatenation) runs, so its device copy can only go
+    away if the forward pass itself lets go of the memory.  Every torch call
+    of the forward passes through here:
+
+    * after the op that produces a swapped branch tensor (its autograd node's
+      rank), the D2H starts (one swap-out per tensor, shared with the
+      saved-tensor path when autograd also saves it — fuse_swap_outs,
+      rewriter.py:294-334);
+    * after the last forward op the rewrite left reading the device copy, the
+      tensor's storage is resized to 0 bytes: the block returns to the pool
+      once the D2H lands (lms_swap_out holds it) while every Python reference
+      and saved alias stays valid;
+    * after the control op's node (rewriter.py:455-477) the storage is
+      re-allocated and the H2D issued; an op reading a freed storage first
+      makes the compute stream wait for its swap-in (issuing it if its control
+      op never ran).
+    """
+
+    def __init__(self, ex: "SwapExecutor", issue_saved):
+        super().__init__()
+        plan = ex.plan
+        self.ex, self.ctx = ex, ex.ctx
+        self.issue_saved = issue_saved   # (saved idx, tensor) -> handle, shared with the pack hook
+        self.groups = [plan.groups[g] for g in plan.fwd_groups]
+        self.by_prod, self.by_release, self.by_trigger = {}, {}, {}
+        for g in self.groups:
+            self.by_prod.setdefault(g.producer_rank, []).append(g)
+            self.by_release.setdefault(g.release_rank, []).append(g)
+            if g.trigger_kind == "forward":
+                self.by_trigger.setdefault(g.trigger, []).append(g)
+        self.ranks = set(self.by_prod) | set(self.by_release) | set(self.by_trigger)
+        self.seq0 = None
+        self.state = {}      # tensor id -> dict(t, h, phase, key)
+        self.freed = {}      # storage key -> tensor id
+        self.n_freed = 0
+
+    def _post(self, r, t):
+        ctx, st = self.ctx, self.state
+        for g in self.by_prod.get(r, ()):
+            if g.tensor in st:
+                continue
+            whole = (t.storage_offset() == 0 and t.is_contiguous()
+                     and t.numel() * t.element_size() == t.untyped_storage().nbytes())
+            if not whole:
+                st[g.tensor] = {"phase": "kept"}
+                continue
+            h = self.issue_saved(g.saved, t)
+            st[g.tensor] = {"t": t, "h": h, "phase": "out", "eager": g.trigger_kind == "eager"}
+        for g in self.by_release.get(r, ()):
+            x = st.get(g.tensor)
+            if x is None or x["phase"] != "out" or x["eager"]:
+                continue
+            stor = x["t"].untyped_storage()
+            x["nbytes"], x["key"] = stor.nbytes(), stor._cdata
+            stor.resize_(0)     # the pool reuses the block once the D2H has landed
+            x["phase"] = "freed"
+            self.freed[x["key"]] = g.tensor
+            self.n_freed += 1
+        for g in self.by_trigger.get(r, ()):
+            x = st.get(g.tensor)
+            if x is None:
+                continue
+            if x["phase"] == "freed":
+                self._swap_in(x)
+            elif x["phase"] == "out":
+                x["eager"] = True    # control op before the release point: keep it resident
+
+    def _swap_in(self, x):
+        x["t"].untyped_storage().resize_(x["nbytes"])
+        self.ctx.swap_in(x["h"], dst=x["t"], trigger_stream=torch.cuda.current_stream())
+        x["phase"] = "in"
+
+    def __torch_function__(self, func, types, args=(), kwargs=None):
+        kwargs = kwargs or {}
+        if self.freed:
+            for a in tree_flatten((args, kwargs))[0]:
+                if isinstance(a, torch.Tensor):
+                    tid = self.freed.get(a.untyped_storage()._cdata)
+                    if tid is not None:
+                        x = self.state[tid]
+                        if x["phase"] == "freed":
+                            self._swap_in(x)
+                        self.ctx.wait(x["h"], torch.cuda.current_stream())
+                        x["phase"] = "restored"
+                        del self.freed[x["key"]]
+        out = func(*args, **kwargs)
+        seen = set()
+        for t in tree_flatten(out)[0]:
+            if isinstance(t, torch.Tensor) and t.grad_fn is not None:
+                seq = t.grad_fn._sequence_nr()
+                if self.seq0 is None:
+                    self.seq0 = seq
+                r = seq - self.seq0
+                if r in self.ranks and r not in seen:
+                    seen.add(r)
+                    self._post(r, t)
+        return out
+
+    def finish(self):
+        """End of forward: anything still freed is restored (its consumer never ran)."""
+        for tid in list(self.freed.values()):
+            x = self.state[tid]
+            if x["phase"] == "freed":
+                self._swap_in(x)
+            self.ctx.wait(x["h"], torch.cuda.current_stream())
+            x["phase"] = "restored"
+        self.freed.clear()
 
 
 class _SwapRef:
@@ -553,6 +752,11 @@ class SwapExecutor:
                 # leak its activations)
                 return t.detach()
             h = handles.get(si)
+            if h is not None and (h.shape != tuple(t.shape) or h.restore_strides != tuple(t.stride())):
+                # a branch swap-out of another view of it: autograd's copy is its own
+                old = handles.pop(si)
+                handles[("fwd", old.id)] = old
+                h = None
             if h is None:
                 h = ctx.swap_out(t, self._codec_for(si, t), stream_of())
                 handles[si] = h
@@ -580,11 +784,29 @@ class SwapExecutor:
                 group_tensor.pop(gid, None)  # the consumer node holds it until it finishes
             return t
 
+        def issue_saved(si, t):
+            """The swap-out of a branch tensor: the saved-tensor path's handle when
+            autograd saves it too (same layout), else a new one."""
+            h = handles.get(si) if si >= 0 else None
+            if h is not None and h.shape == tuple(t.shape) and h.restore_strides == tuple(t.stride()):
+                return h
+            h = ctx.swap_out(t, self._codec_for(si, t) if si >= 0 else "ce", stream_of())
+            key = si if si >= 0 and si not in handles else ("fwd", h.id)
+            handles[key] = h
+            return h
+
+        fwd = _ForwardSwaps(self, issue_saved) if plan.fwd_groups else None
+        self.forward_swaps = fwd
         hooks = []
         loss = None
         try:
             with torch.autograd.graph.saved_tensors_hooks(pack, unpack):
-                loss = forward_fn()
+                if fwd is None:
+                    loss = forward_fn()
+                else:
+                    with fwd:
+                        loss = forward_fn()
+                    fwd.finish()
             if k_counter[0] != plan.n_packs:
                 raise RuntimeError(f"step saved {k_counter[0]} tensors but the plan was captured with "
                                    f"{plan.n_packs}; re-capture the plan for this model/step")
@@ -614,6 +836,8 @@ class SwapExecutor:
                 hk.remove()
             hooks.clear()
             group_tensor.clear()
+            if fwd is not None:
+                fwd.state.clear()
             for h in handles.values():
                 ctx.release(h)
             handles.clear()
@@ -652,8 +876,15 @@ class LMS:
         """Trace one step at (x, y) — no optimizer update — and build the swap plan."""
         self.optimizer.zero_grad(set_to_none=True)
         persistent = list(self.model.parameters()) + list(self.model.buffers()) + [x, y]
+        # the traced step is not a training step: module buffers it updates
+        # (BatchNorm running statistics, num_batches_tracked) are put back
+        kept = [(b, b.detach().clone()) for b in self.model.buffers()]
         self.graph, self.meta = capture_graph(lambda: self.loss_fn(self.model(x), y), self.min_swap_bytes,
                                               persistent)
+        with torch.no_grad():
+            for b, v in kept:
+                b.copy_(v)
+        del kept
         self.optimizer.zero_grad(set_to_none=True)
         self.replan(self.cfg)
         return self.plan

@@ -146,3 +146,42 @@ def test_plan_window_moves_respects_room_and_issue_order():
     # no room at all: nothing moves
     live2 = np.full(100, 20.0)
     assert plan_window_moves(live2, node_clock, issue, cands, trig, limit=20.0) == []
+
+
+def test_swap_branches_plans_forward_swaps():
+    """swap_branches (rewriter.py:231) swaps fwd->fwd edges such as U-Net skip
+    tensors; the plan maps them to forward-side swap-in groups (the round-1
+    build_plan raised KeyError on them)."""
+    from paper_1807_02037_b200.workloads import unet3d
+    torch.manual_seed(0)
+    m = unet3d(base=4, depth=2)
+    x = torch.randn(1, 1, 16, 16, 16)
+    y = torch.randint(0, 2, (1, 16, 16, 16))
+    g, meta = capture_graph(lambda: torch.nn.functional.cross_entropy(m(x), y), min_swap_bytes=0)
+    assert validate(g) == []
+    assert meta["fwd_ranks_ok"]
+    # forward outputs carry their bytes, so branch tensors have real sizes
+    fwd_fwd = [e for e in g.edges if e.action is EdgeAction.READ and g.node(e.src).phase is Phase.FORWARD
+               and g.node(e.dst).phase is Phase.FORWARD and g.tensor(e.tensor).size_bytes > 0]
+    assert len(fwd_fwd) > 10
+    plain = build_plan(g, meta, RewriteConfig(ctrld_strategy="chain_rule"), capture_batch=1)
+    assert plain.fwd_groups == []
+    cfg = RewriteConfig(swap_branches=True, branch_threshold=20, lb=1)
+    plan = build_plan(g, meta, cfg, capture_batch=1)
+    assert plan.report.swap_ins_added > plain.report.swap_ins_added
+    fg = [plan.groups[i] for i in plan.fwd_groups]
+    assert fg, "the skip concatenations' inputs are branch swaps"
+    order = {}
+    from paper_1807_02037_b200 import topo_order
+    order = topo_order(g)
+    for grp in fg:
+        assert grp.fwd_consumers and grp.release_rank >= grp.producer_rank
+        assert all(c > grp.release_rank for c in grp.fwd_consumers)
+        if grp.trigger_kind == "forward":
+            assert grp.release_rank <= grp.trigger < min(grp.fwd_consumers) or grp.trigger < grp.release_rank
+        # the swapped edge jumps more than branch_threshold levels (strict >)
+        t = g.tensor(grp.tensor)
+        cons = [e.dst for e in g.consumer_edges(grp.tensor) if meta["F"].get(e.dst) in grp.fwd_consumers]
+        assert all(order[d] - order[t.producer] > 20 for d in cons)
+    # every group id indexes plan.groups
+    assert [grp.gid for grp in plan.groups] == list(range(len(plan.groups)))
