@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--fuse-distance", type=int, default=12,
                     help="RewriteConfig.swapin_fuse_distance (12: a tensor read by two backward ops "
                          "a few levels apart is swapped in once)")
+    ap.add_argument("--branches", action="store_true",
+                    help="RewriteConfig.swap_branches: also swap forward->forward tensors (U-Net skips)")
+    ap.add_argument("--branch-threshold", type=int, default=20,
+                    help="RewriteConfig.branch_threshold (the paper's 3DUnet run used 20, PAPER.md:1064)")
     ap.add_argument("--b0", type=int, default=0, help="skip bisection and use this no-swap batch")
     ap.add_argument("--n-tensors", type=int, default=0,
                     help="swap only the first n candidate tensors (rewrite BFS order); -1 = all; "
@@ -378,7 +382,8 @@ def main():
         cap_scale = (size / cap_size) ** 3
     else:
         xc, yc = batch(cap_b)
-    cfg0 = RewriteConfig(lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
+    cfg0 = RewriteConfig(lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy, swap_branches=args.branches,
+                                 branch_threshold=args.branch_threshold,
                          fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance)
     codec = args.codec
     # tensors under 64 KiB at the capture size stay on the device
@@ -418,7 +423,8 @@ def main():
 
     def try_swap(nb, n_tensors):
         """Run ``warmup`` swapped steps at batch nb; True if they fit the budget."""
-        cfg = RewriteConfig(n_tensors=n_tensors, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
+        cfg = RewriteConfig(n_tensors=n_tensors, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy, swap_branches=args.branches,
+                                 branch_threshold=args.branch_threshold,
                             fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance)
         lms.replan(cfg)
         lms.static_plan = False   # fit probes run on the dynamic pool; the timed run plans
@@ -517,7 +523,8 @@ def main():
         """Warm-up + exactly ``args.steps`` timed swapped steps; None if the budget is hit."""
         nonlocal st0, clk, tuned, prepared, extra_warmup
         lms.replan(RewriteConfig(n_tensors=n_use if n_use < N else -1, lb=args.lb, ub=args.ub,
-                                 ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
+                                 ctrld_strategy=args.strategy, swap_branches=args.branches,
+                                 branch_threshold=args.branch_threshold, fuse_swapins=args.fuse_swapins,
                                  swapin_fuse_distance=args.fuse_distance))
         clocks = Clocks(local)
         tuned = {}
@@ -570,7 +577,8 @@ def main():
     if args.autotune:   # empirical control-op window (LMS.autotune); the timed run uses the winner
         n0 = min(ok_ns)
         lms.replan(RewriteConfig(n_tensors=n0 if n0 < N else -1, lb=args.lb, ub=args.ub,
-                                 ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
+                                 ctrld_strategy=args.strategy, swap_branches=args.branches,
+                                 branch_threshold=args.branch_threshold, fuse_swapins=args.fuse_swapins,
                                  swapin_fuse_distance=args.fuse_distance))
         lms.static_plan = False
         tune = lms.autotune(xs, ys, lbs=(1, 2, 3, 5, 8), steps=2)
@@ -596,7 +604,8 @@ def main():
                 log(f"[bench] joint search budget spent; skipping n_tensors={n}")
                 break
             lms.replan(RewriteConfig(n_tensors=n if n < N else -1, lb=args.lb, ub=args.ub,
-                                     ctrld_strategy=args.strategy, fuse_swapins=args.fuse_swapins,
+                                     ctrld_strategy=args.strategy, swap_branches=args.branches,
+                                 branch_threshold=args.branch_threshold, fuse_swapins=args.fuse_swapins,
                                      swapin_fuse_distance=args.fuse_distance))
             try:
                 info = lms.tune_windows(xs, ys)
@@ -661,7 +670,8 @@ def main():
     same_batch = None
     if b0 > 0 and args.same_batch:
         x0, y0 = batch(b0, seed=3)
-        lms.replan(RewriteConfig(n_tensors=-1, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy,
+        lms.replan(RewriteConfig(n_tensors=-1, lb=args.lb, ub=args.ub, ctrld_strategy=args.strategy, swap_branches=args.branches,
+                                 branch_threshold=args.branch_threshold,
                                  fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance))
         for _ in range(max(3, args.warmup)):
             lms.step(x0, y0)
@@ -753,6 +763,7 @@ def main():
                    "l2": "inputs (>=450 MB/step) exceed L2; no flush",
                    "rewrite": {"lb": args.lb, "ub": args.ub, "ctrld_strategy": args.strategy,
                                "fuse_swapins": args.fuse_swapins, "n_tensors": plan.report.tensors_swapped,
+                               "swap_branches": args.branches, "branch_threshold": args.branch_threshold,
                                "tune_windows": args.tune_windows, "swap_ins_moved": (tuned or {}).get("moved", 0)},
                    "codec": args.codec},
         "no_swap": {"batch": b0, "img_s": round(noswap_ips, 2) if noswap_ips else None,
@@ -761,6 +772,7 @@ def main():
                      "note": "img/s at B0 without swap / img/s at 4.7xB0 with swap - 1",
                      "same_batch": same_batch},
         "swap": {"tensors_swapped": plan.report.tensors_swapped, "swap_ins": len(plan.groups),
+                 "forward_swap_ins": len(plan.fwd_groups),
                  "control_edges": plan.report.control_edges_added,
                  "d2h_bytes_per_step": d2h_b // steps, "h2d_bytes_per_step": h2d_b // steps,
                  "logical_d2h_per_step": st1["d2h_logical_bytes"] // steps,
