@@ -481,7 +481,7 @@ def main():
             probe = (lo_n + hi_n) // 2
     if not fitted:
         # the paper's "max batch with TFLMS": bisect between B0 and the target
-        lo_b, hi_b = b0, bs
+        lo_b, hi_b = max(b0, 1), bs
         while hi_b - lo_b > max(4, b0 // 16):
             mid = (lo_b + hi_b) // 2
             if try_swap(mid, -1):

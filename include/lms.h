@@ -51,10 +51,14 @@ enum {
 /* Transfer codecs for swap-out.  RAW_CE moves the tensor's storage span with
  * the copy engine (packing first only when the view is not dense).  RAW_SM
  * moves it with an SM kernel writing straight into mapped pinned memory
- * (fused pack for strided views).  ZVC is lossless zero-value compression:
- * an SM kernel writes a bitmask plus the nonzero words into pinned memory,
- * and the swap-in decodes after a copy-engine H2D of the compressed bytes. */
-enum { LMS_CODEC_RAW_CE = 0, LMS_CODEC_RAW_SM = 1, LMS_CODEC_ZVC = 2 };
+ * (fused pack for strided views).  ZVC is a lossless tile codec over 32-bit
+ * words: one SM kernel pass writes, per 16 KiB tile, either the words or a
+ * zero bitmask plus the nonzero words straight into pinned memory, and the
+ * swap-in decodes straight out of it (only encoded bytes cross the link).
+ * ZX is ZVC plus exponent planes: a tile may also store each word's low 24
+ * bits and its top byte coded in the tile's narrow exponent band (k bits +
+ * a sign bit unless all signs agree) — lossless, for dense fp32 tensors. */
+enum { LMS_CODEC_RAW_CE = 0, LMS_CODEC_RAW_SM = 1, LMS_CODEC_ZVC = 2, LMS_CODEC_ZX = 3 };
 
 typedef struct lms_ctx lms_ctx;
 typedef struct lms_handle lms_handle;
@@ -90,7 +94,7 @@ typedef struct {
   double alloc_wait_ms;    /* host time allocations spent waiting for swap-out copies */
   double host_grow_ms;     /* host time pinning new host-pool chunks (cudaHostAlloc) */
   uint64_t n_host_grow;    /* pinned chunks added */
-  uint64_t n_scratch_grow; /* ZVC scratch reallocations */
+  uint64_t n_scratch_grow; /* always 0 (the one-pass ZVC v3 codec has no scratch); kept for the ABI */
   double unmap_ms, map_ms, access_ms;  /* pool_driver_ms split by driver call */
 } lms_stats_t;
 
@@ -216,12 +220,15 @@ int lms_pack(lms_ctx* ctx, void* dst, const void* src, const int64_t* sizes,
 /* dst (strided view) <- src (contiguous) */
 int lms_unpack(lms_ctx* ctx, void* dst, const void* src, const int64_t* sizes,
                const int64_t* strides, int ndim, int elem_size, void* stream);
-/* ZVC codec over `nwords` 32-bit words; encode writes to any device-visible
- * buffer (pinned host included) of at least lms_zvc_bound(nwords) bytes. */
+/* ZVC / ZX codec over `nwords` 32-bit words (exponents != 0: ZX tile forms
+ * allowed); encode writes to any device-visible buffer (pinned host included)
+ * of at least lms_zvc_bound(nwords) bytes, one pass over the source, each
+ * tile into its own fixed 16 KiB slot.  Stream format: kernels.cuh (ZVC v3). */
 size_t lms_zvc_bound(size_t nwords);
-int lms_zvc_encode(lms_ctx* ctx, const void* src, size_t nwords, void* dst, void* stream);
+int lms_zvc_encode(lms_ctx* ctx, const void* src, size_t nwords, void* dst, int exponents, void* stream);
 int lms_zvc_decode(lms_ctx* ctx, const void* enc, size_t nwords, void* dst, void* stream);
-/* bytes used by an encoded stream whose header is host-readable */
+/* bytes an encoded stream put on the wire (header + tile table + chunks);
+ * the stream must be host-readable */
 int lms_zvc_encoded_size(const void* enc_host, size_t* out);
 
 /* ---- measured simulation (replaces sim.py:139-476's modelled op) ----------- */

@@ -10,9 +10,9 @@
 //                 generic paths)
 //   copy16        device<->pinned-host streaming copy driven by SMs
 //                 (zero-copy: the "kernel" transfer engine)
-//   zvc_*         lossless zero-value compression of 32-bit words:
-//                 count -> scan -> encode straight into pinned memory, and
-//                 decode from an H2D-staged stream back into HBM
+//   zvc_*         lossless tile codec of 32-bit words (zero masks and
+//                 exponent planes), one pass straight into pinned memory,
+//                 decoded straight out of it
 #pragma once
 
 #include <cstdint>
@@ -291,168 +291,62 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // -------------------------------------------------------------------------
-// ZVC: lossless zero-value compression over 32-bit words (stream format v2).
+// ZVC v3: lossless tile codec over 32-bit words, one pass over HBM.
 //
-// A swapped activation is compressed on its way out (SM kernels writing
-// straight into mapped pinned memory) and decompressed on its way in (SM
-// kernels reading straight out of pinned memory), so only the compressed
-// bytes cross the host link and no device staging buffer is needed.
+// A swapped activation is encoded on its way out by SM kernels writing
+// straight into mapped pinned memory, and decoded on its way in by SM
+// kernels reading straight out of it, so only the encoded bytes cross the
+// host link and no device staging buffer is taken from the budget.
 //
-// Stream layout (bytes from the start; every region 16 B aligned):
-//   [0, 64)                  header {magic "ZVC2", mode, nwords, ntiles, total_nnz, bytes, data_pos}
-//   [64, data_pos)           u32 chunk offsets, ntiles+1 entries, in 16 B units from data_pos
-//   [data_pos, bytes)        one chunk per tile, in tile order:
-//                              128-word bitmask (bit j of word s: word 32s+j of the tile is nonzero)
-//                              the tile's nonzero words in order, zero-padded to 16 B
-// A tile is 4096 words (16 KiB).  mode 0 = raw: the words follow the header
-// directly; the scan kernel picks it on the device when compression would
-// not shrink the stream.  Words past nwords in the last tile encode as zero.
+// Every 4096-word (16 KiB) tile picks the smallest of four lossless forms:
+//   RAW   the words
+//   MASK  128-word bitmask (bit j of word s: word 32s+j is nonzero) + the
+//         nonzero words                          (ReLU outputs: ~50 % zeros)
+//   EXPD  every word split into its low 24 bits (3-byte plane) and its top
+//         byte (sign + 7 high exponent bits), the top bytes coded as
+//         (e7 - emin) in k bits plus a sign bit unless the tile's signs agree
+//   EXPM  MASK's bitmask, then EXPD's two planes over the nonzero words only
+// (fp32 activations keep their exponents in a narrow band per tile: k is
+// typically 3-4 of 7 bits, and ReLU outputs need no sign bit.)
+//
+// Stream layout (bytes; every region 16 B aligned):
+//   [0, 64)                     header {magic "ZVC3", flags, nwords, ntiles, table_pos, data_pos}
+//   [64, 64 + 8 ntiles)         per tile {u32 info, u32 bytes}: info = mode | k<<2 | signplane<<6 |
+//                               sign<<7 | emin<<8 | n<<16 (n = words coded: tile words, or nnz)
+//   [data_pos, ...)             tile t's chunk at data_pos + t * 16 KiB (fixed slots: no scan
+//                               pass; only a chunk's own bytes are ever written or read)
+// There is no global pass: a CTA encodes a tile from registers, builds the
+// chunk in shared memory and stores it with one bulk copy.
 
 constexpr int kZvcTileWords = 4096;
-constexpr int kZvcMaskWords = kZvcTileWords / 32;                  // 128
-constexpr int kZvcChunkWords = kZvcMaskWords + kZvcTileWords;       // worst-case chunk (4224 words)
-constexpr int kZvcSmemBytes = 2 * kZvcChunkWords * 4;               // double-buffered chunks
-constexpr uint32_t kZvcMagic = 0x3243565Au;                          // "ZVC2"
+constexpr int kZvcMaskWords = kZvcTileWords / 32;                 // 128
+constexpr uint32_t kZvcSlotBytes = kZvcTileWords * 4;             // 16 KiB
+constexpr int kZvcBufBytes = kZvcSlotBytes + 512;                 // chunk buffer (+ scratch slack)
+constexpr int kZvcSmemBytes = 2 * kZvcBufBytes;                   // double-buffered
+constexpr uint32_t kZvcMagic = 0x3343565Au;                       // "ZVC3"
+enum { kZRaw = 0, kZMask = 1, kZExpD = 2, kZExpM = 3 };
 
 struct ZvcHeader {
-  uint32_t magic, mode;
-  uint64_t nwords, ntiles, total_nnz, bytes, data_pos;
-  uint64_t pad[2];
+  uint32_t magic, flags;
+  uint64_t nwords, ntiles, table_pos, data_pos;
+  uint64_t pad[3];
 };
 static_assert(sizeof(ZvcHeader) == 64, "header is 64 bytes");
+
+struct ZvcTile {
+  uint32_t info, bytes;
+};
 
 __host__ __device__ inline uint64_t zvc_tiles(uint64_t nwords) {
   return (nwords + kZvcTileWords - 1) / kZvcTileWords;
 }
-__host__ __device__ inline uint64_t zvc_data_pos(uint64_t ntiles) { return 64 + ((ntiles + 1 + 3) / 4) * 16; }
-__host__ __device__ inline uint64_t zvc_raw_bytes(uint64_t nwords) { return 64 + (nwords * 4 + 15) / 16 * 16; }
+__host__ __device__ inline uint64_t zvc_data_pos(uint64_t ntiles) { return 64 + (ntiles * 8 + 15) / 16 * 16; }
+__host__ __device__ inline uint32_t zvc_pad16(uint64_t b) { return uint32_t((b + 15) / 16 * 16); }
+// worst case: every chunk raw; the last tile's slot only needs its own words
 __host__ __device__ inline uint64_t zvc_bound(uint64_t nwords) {
   const uint64_t t = zvc_tiles(nwords);
-  const uint64_t a = zvc_data_pos(t) + t * uint64_t(kZvcChunkWords) * 4;  // every tile dense
-  const uint64_t b = zvc_raw_bytes(nwords);
-  return a > b ? a : b;
-}
-
-// pass 1: nonzero words per tile (HBM read; the source stays on the device)
-__global__ void __launch_bounds__(256) zvc_count_kernel(const uint32_t* __restrict__ src, uint64_t nwords,
-                                                        uint32_t* __restrict__ counts) {
-  __shared__ uint32_t red[8];
-  const uint64_t ntiles = zvc_tiles(nwords);
-  const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint64_t base = t * kZvcTileWords;
-    uint32_t c = 0;
-    if (vec && base + kZvcTileWords <= nwords) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(src + base);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint4 v = ld_stream(s4 + threadIdx.x + k * 256);
-        c += (v.x != 0) + (v.y != 0) + (v.z != 0) + (v.w != 0);
-      }
-    } else {
-      const uint64_t end = base + kZvcTileWords < nwords ? base + kZvcTileWords : nwords;
-      for (uint64_t i = base + threadIdx.x; i < end; i += 256) c += src[i] != 0;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t s = 0;
-      for (int w = 0; w < 8; ++w) s += red[w];
-      counts[t] = s;
-    }
-    __syncthreads();
-  }
-}
-
-// pass 2 (one CTA): chunk sizes -> exclusive offsets; header and offset table
-// go to `out`; offsets[ntiles+1] carries the mode to the encode kernel.
-__global__ void __launch_bounds__(1024) zvc_scan_kernel(const uint32_t* __restrict__ counts, uint64_t nwords,
-                                                        uint32_t* __restrict__ offsets, char* __restrict__ out) {
-  __shared__ uint32_t warp_tot[32];
-  __shared__ uint32_t carry;
-  __shared__ unsigned long long nnz_tot;
-  const uint64_t ntiles = zvc_tiles(nwords);
-  if (threadIdx.x == 0) {
-    carry = 0;
-    nnz_tot = 0;
-  }
-  __syncthreads();
-  uint64_t my_nnz = 0;
-  for (uint64_t base = 0; base < ntiles; base += 1024) {
-    const uint64_t i = base + threadIdx.x;
-    const uint32_t nnz = i < ntiles ? counts[i] : 0;
-    my_nnz += nnz;
-    const uint32_t v = i < ntiles ? kZvcMaskWords / 4 + (nnz + 3) / 4 : 0;  // chunk size, 16 B units
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if ((threadIdx.x & 31) >= o) x += y;
-    }
-    if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      uint32_t w = warp_tot[threadIdx.x];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (threadIdx.x >= o) w += y;
-      }
-      warp_tot[threadIdx.x] = w;  // inclusive
-    }
-    __syncthreads();
-    const uint32_t warp_base = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0;
-    const uint32_t excl = carry + warp_base + x - v;
-    if (i < ntiles) offsets[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
-  }
-  atomicAdd(&nnz_tot, (unsigned long long)my_nnz);
-  __syncthreads();
-  uint32_t* table = reinterpret_cast<uint32_t*>(out + 64);
-  if (threadIdx.x == 0) {
-    ZvcHeader h{};
-    h.magic = kZvcMagic;
-    h.nwords = nwords;
-    h.ntiles = ntiles;
-    h.total_nnz = nnz_tot;
-    h.data_pos = zvc_data_pos(ntiles);
-    const uint64_t zbytes = h.data_pos + uint64_t(carry) * 16;
-    const uint64_t rbytes = zvc_raw_bytes(nwords);
-    h.mode = zbytes < rbytes ? 1u : 0u;
-    h.bytes = h.mode ? zbytes : rbytes;
-    offsets[ntiles] = carry;
-    offsets[ntiles + 1] = h.mode;
-    const uint4* hs = reinterpret_cast<const uint4*>(&h);
-    uint4* ho = reinterpret_cast<uint4*>(out);
-    for (int k = 0; k < 4; ++k) ho[k] = hs[k];
-    if (h.mode) table[ntiles] = carry;
-  }
-  __syncthreads();
-  if (offsets[ntiles + 1])
-    for (uint64_t i = threadIdx.x; i < ntiles; i += 1024) table[i] = offsets[i];
-}
-
-// raw mode body: 16 B words after the header (grid-stride), word tail by CTA 0
-__device__ __forceinline__ void zvc_raw_copy(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
-                                             uint64_t nwords) {
-  const uint64_t n16 = nwords / 4;
-  uint4* d4 = reinterpret_cast<uint4*>(dst);
-  const uint4* s4 = reinterpret_cast<const uint4*>(src);
-  const uint64_t nth = uint64_t(gridDim.x) * blockDim.x;
-  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + 3 * nth < n16; i += 4 * nth) {
-    uint4 a = ld_stream(s4 + i), b = ld_stream(s4 + i + nth);
-    uint4 c = ld_stream(s4 + i + 2 * nth), e = ld_stream(s4 + i + 3 * nth);
-    st_stream(d4 + i, a); st_stream(d4 + i + nth, b);
-    st_stream(d4 + i + 2 * nth, c); st_stream(d4 + i + 3 * nth, e);
-  }
-  for (; i < n16; i += nth) st_stream(d4 + i, ld_stream(s4 + i));
-  if (blockIdx.x == 0)
-    for (uint64_t k = n16 * 4 + threadIdx.x; k < nwords; k += blockDim.x) dst[k] = src[k];
+  if (t == 0) return 64;
+  return zvc_data_pos(t) + (t - 1) * kZvcSlotBytes + zvc_pad16(4 * (nwords - (t - 1) * kZvcTileWords));
 }
 
 // exclusive scan of the 128 per-segment popcounts in seg[] (warp 0); seg[128] = total
@@ -472,92 +366,225 @@ __device__ __forceinline__ void zvc_seg_scan(uint32_t* seg, int lane) {
   if (lane == 31) seg[kZvcMaskWords] = x;
 }
 
-// pass 3: per tile, bitmask + compacted nonzeros assembled in shared memory,
-// then one bulk store of the whole chunk (TMA when use_bulk, else 16 B STG).
-// Double-buffered: tile k+1 is compacted while tile k's chunk is in flight.
-__global__ void __launch_bounds__(256) zvc_encode_kernel(const uint32_t* __restrict__ src, uint64_t nwords,
-                                                         const uint32_t* __restrict__ offsets,
-                                                         char* __restrict__ out, int use_bulk) {
-  extern __shared__ __align__(128) uint32_t zsm[];
-  __shared__ uint32_t seg[kZvcMaskWords + 1];
-  const uint64_t ntiles = zvc_tiles(nwords);
-  if (offsets[ntiles + 1] == 0) {  // raw mode
-    zvc_raw_copy(reinterpret_cast<uint32_t*>(out + 64), src, nwords);
-    return;
+__device__ __forceinline__ uint32_t zvc_nbits(uint32_t r) { return r ? 32u - __clz(r) : 0u; }
+
+// exponent planes: word p's low 24 bits at byte 3p of `lo`, its code at bit p*b of `hi`
+__device__ __forceinline__ void zvc_put_exp(unsigned char* lo, uint32_t* hi, uint32_t p, uint32_t w, uint32_t k,
+                                            uint32_t sp, uint32_t emin) {
+  lo[3 * p] = uint8_t(w);
+  lo[3 * p + 1] = uint8_t(w >> 8);
+  lo[3 * p + 2] = uint8_t(w >> 16);
+  const uint32_t b = k + sp;
+  if (b == 0) return;
+  const uint32_t code = (((w >> 24) & 0x7Fu) - emin) | (sp ? (w >> 31) << k : 0u);
+  const uint32_t o = p * b, q = o >> 5, sh = o & 31u;
+  atomicOr(hi + q, code << sh);
+  if (sh + b > 32) atomicOr(hi + q + 1, code >> (32 - sh));
+}
+
+__device__ __forceinline__ uint32_t zvc_get_exp(const unsigned char* lo, const uint32_t* hi, uint32_t p, uint32_t k,
+                                                uint32_t sp, uint32_t sconst, uint32_t emin) {
+  const uint32_t low = uint32_t(lo[3 * p]) | uint32_t(lo[3 * p + 1]) << 8 | uint32_t(lo[3 * p + 2]) << 16;
+  const uint32_t b = k + sp;
+  uint32_t code = 0;
+  if (b) {
+    const uint32_t o = p * b, q = o >> 5, sh = o & 31u;
+    code = hi[q] >> sh;
+    if (sh + b > 32) code |= hi[q + 1] << (32 - sh);
   }
+  const uint32_t e7 = emin + (code & ((1u << k) - 1u));
+  const uint32_t s = sp ? (code >> k) & 1u : sconst;
+  return ((s << 7 | e7) << 24) | low;
+}
+
+// One pass: per tile, statistics of the 4096 words held in registers pick the
+// form, the chunk is assembled in shared memory and leaves with one bulk
+// store (TMA when use_bulk, else 16 B STG) into its fixed slot.  Double-
+// buffered: tile k+1 is built while tile k's chunk is in flight.
+__global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __restrict__ src, uint64_t nwords,
+                                                         char* __restrict__ out, int use_bulk, int allow_exp) {
+  extern __shared__ __align__(128) unsigned char zsm[];
+  __shared__ uint32_t seg[kZvcMaskWords + 1];
+  __shared__ uint32_t red[8][9];
+  __shared__ uint32_t pick[3];   // info, bytes, hi-plane offset
+  const uint64_t ntiles = zvc_tiles(nwords);
+  const uint64_t dpos = zvc_data_pos(ntiles);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ZvcHeader h{};
+    h.magic = kZvcMagic;
+    h.flags = uint32_t(allow_exp != 0);
+    h.nwords = nwords;
+    h.ntiles = ntiles;
+    h.table_pos = 64;
+    h.data_pos = dpos;
+    const uint4* hs = reinterpret_cast<const uint4*>(&h);
+    uint4* ho = reinterpret_cast<uint4*>(out);
+    for (int k = 0; k < 4; ++k) ho[k] = hs[k];
+  }
+  ZvcTile* table = reinterpret_cast<ZvcTile*>(out + 64);
+  char* data = out + dpos;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  char* data = out + zvc_data_pos(ntiles);
+  const uint32_t lt = (1u << lane) - 1u;
   int buf = 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
-    uint32_t* chunk = zsm + buf * kZvcChunkWords;
+    unsigned char* chunk = zsm + buf * kZvcBufBytes;
+    uint32_t* cw = reinterpret_cast<uint32_t*>(chunk);
     if (use_bulk && threadIdx.x == 0) bulk_wait_read<1>();  // the store that last read this buffer
     __syncthreads();
     const uint64_t base = t * kZvcTileWords;
+    const uint32_t nvalid = uint32_t(nwords - base < kZvcTileWords ? nwords - base : kZvcTileWords);
     uint32_t w16[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const uint64_t i = base + r * 256 + threadIdx.x;
       w16[r] = i < nwords ? __ldg(src + i) : 0u;
     }
+    // per-tile statistics: nonzeros, and the top-byte ranges over all / nonzero words
+    uint32_t nnz = 0, mn_a = 127, mx_a = 0, or_a = 0, and_a = 1, mn_z = 127, mx_z = 0, or_z = 0, and_z = 1;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint32_t m = __ballot_sync(0xffffffffu, w16[r] != 0);
-      if (lane == 0) {
-        chunk[r * 8 + warp] = m;
-        seg[r * 8 + warp] = __popc(m);
+      const uint32_t v = w16[r], e7 = (v >> 24) & 0x7Fu, s = v >> 31;
+      if (uint32_t(r * 256 + threadIdx.x) < nvalid) {
+        mn_a = min(mn_a, e7);
+        mx_a = max(mx_a, e7);
+        or_a |= s;
+        and_a &= s;
+      }
+      if (v) {
+        ++nnz;
+        mn_z = min(mn_z, e7);
+        mx_z = max(mx_z, e7);
+        or_z |= s;
+        and_z &= s;
       }
     }
-    __syncthreads();
-    if (warp == 0) zvc_seg_scan(seg, lane);
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const uint32_t m = chunk[r * 8 + warp];
-      if (w16[r] != 0) chunk[kZvcMaskWords + seg[r * 8 + warp] + __popc(m & ((1u << lane) - 1u))] = w16[r];
+    nnz = __reduce_add_sync(0xffffffffu, nnz);
+    mn_a = __reduce_min_sync(0xffffffffu, mn_a);
+    mx_a = __reduce_max_sync(0xffffffffu, mx_a);
+    or_a = __reduce_or_sync(0xffffffffu, or_a);
+    and_a = __reduce_and_sync(0xffffffffu, and_a);
+    mn_z = __reduce_min_sync(0xffffffffu, mn_z);
+    mx_z = __reduce_max_sync(0xffffffffu, mx_z);
+    or_z = __reduce_or_sync(0xffffffffu, or_z);
+    and_z = __reduce_and_sync(0xffffffffu, and_z);
+    if (lane == 0) {
+      red[warp][0] = nnz; red[warp][1] = mn_a; red[warp][2] = mx_a; red[warp][3] = or_a; red[warp][4] = and_a;
+      red[warp][5] = mn_z; red[warp][6] = mx_z; red[warp][7] = or_z; red[warp][8] = and_z;
     }
-    const uint32_t n = seg[kZvcMaskWords];
-    const uint32_t padded = (n + 3) & ~3u;
-    if (threadIdx.x < padded - n) chunk[kZvcMaskWords + n + threadIdx.x] = 0u;
-    const uint32_t bytes = (kZvcMaskWords + padded) * 4;
-    char* dst = data + uint64_t(offsets[t]) * 16;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 1; k < 8; ++k) {
+        red[0][0] += red[k][0];
+        red[0][1] = min(red[0][1], red[k][1]); red[0][2] = max(red[0][2], red[k][2]);
+        red[0][3] |= red[k][3]; red[0][4] &= red[k][4];
+        red[0][5] = min(red[0][5], red[k][5]); red[0][6] = max(red[0][6], red[k][6]);
+        red[0][7] |= red[k][7]; red[0][8] &= red[k][8];
+      }
+      const uint32_t z = red[0][0];
+      uint32_t mode = kZRaw, bytes = zvc_pad16(4ull * nvalid), n = nvalid, k = 0, sp = 0, sc = 0, em = 0, hoff = 0;
+      const uint32_t bm = 512 + zvc_pad16(4ull * z);
+      if (bm < bytes) mode = kZMask, bytes = bm, n = z;
+      if (allow_exp) {
+        const uint32_t kd = zvc_nbits(red[0][2] - red[0][1]), sd = red[0][3] != red[0][4];
+        const uint32_t bd = zvc_pad16(3ull * nvalid) + zvc_pad16((uint64_t(nvalid) * (kd + sd) + 7) / 8);
+        if (bd < bytes) mode = kZExpD, bytes = bd, n = nvalid, k = kd, sp = sd, sc = red[0][3], em = red[0][1],
+                        hoff = zvc_pad16(3ull * nvalid);
+        if (z) {
+          const uint32_t km = zvc_nbits(red[0][6] - red[0][5]), sm = red[0][7] != red[0][8];
+          const uint32_t be = 512 + zvc_pad16(3ull * z) + zvc_pad16((uint64_t(z) * (km + sm) + 7) / 8);
+          if (be < bytes) mode = kZExpM, bytes = be, n = z, k = km, sp = sm, sc = red[0][7], em = red[0][5],
+                          hoff = 512 + zvc_pad16(3ull * z);
+        }
+      }
+      pick[0] = mode | k << 2 | sp << 6 | sc << 7 | em << 8 | n << 16;
+      pick[1] = bytes;
+      pick[2] = hoff;
+    }
+    __syncthreads();
+    const uint32_t info = pick[0], bytes = pick[1], hoff = pick[2];
+    const uint32_t mode = info & 3u, k = (info >> 2) & 15u, sp = (info >> 6) & 1u, em = (info >> 8) & 0x7Fu;
+    if (mode >= kZExpD) {   // the code plane is OR-ed together: clear it (and the padding) first
+      for (uint32_t q = hoff / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
+      const uint32_t lo0 = mode == kZExpM ? 512u : 0u, nlo = 3u * (info >> 16);
+      for (uint32_t b = lo0 + nlo + threadIdx.x; b < hoff; b += 256) chunk[b] = 0;
+    }
+    if (mode == kZMask || mode == kZExpM) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t m = __ballot_sync(0xffffffffu, w16[r] != 0);
+        if (lane == 0) {
+          cw[r * 8 + warp] = m;
+          seg[r * 8 + warp] = __popc(m);
+        }
+      }
+      __syncthreads();
+      if (warp == 0) zvc_seg_scan(seg, lane);
+    }
+    __syncthreads();
+    if (mode == kZRaw) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t j = r * 256 + threadIdx.x;
+        if (j < bytes / 4) cw[j] = w16[r];   // zero past nwords: the padding is deterministic
+      }
+    } else if (mode == kZMask) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t m = cw[r * 8 + warp];
+        if (w16[r] != 0) cw[kZvcMaskWords + seg[r * 8 + warp] + __popc(m & lt)] = w16[r];
+      }
+      const uint32_t z = seg[kZvcMaskWords];
+      if (threadIdx.x < ((z + 3) & ~3u) - z) cw[kZvcMaskWords + z + threadIdx.x] = 0u;
+    } else if (mode == kZExpD) {
+      uint32_t* hi = reinterpret_cast<uint32_t*>(chunk + hoff);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t j = r * 256 + threadIdx.x;
+        if (j < nvalid) zvc_put_exp(chunk, hi, j, w16[r], k, sp, em);
+      }
+    } else {
+      uint32_t* hi = reinterpret_cast<uint32_t*>(chunk + hoff);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t m = cw[r * 8 + warp];
+        if (w16[r] != 0) zvc_put_exp(chunk + 512, hi, seg[r * 8 + warp] + __popc(m & lt), w16[r], k, sp, em);
+      }
+    }
+    char* dst = data + t * kZvcSlotBytes;
     if (use_bulk) {
       fence_proxy_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
         bulk_s2g(dst, chunk, bytes);
         bulk_commit();
+        table[t] = ZvcTile{info, bytes};
       }
     } else {
       __syncthreads();
       const uint4* c4 = reinterpret_cast<const uint4*>(chunk);
       uint4* d4 = reinterpret_cast<uint4*>(dst);
-      for (uint32_t k = threadIdx.x; k < bytes / 16; k += 256) st_stream(d4 + k, c4[k]);
+      for (uint32_t q = threadIdx.x; q < bytes / 16; q += 256) st_stream(d4 + q, c4[q]);
+      if (threadIdx.x == 0) table[t] = ZvcTile{info, bytes};
     }
   }
   if (use_bulk && threadIdx.x == 0) bulk_wait<0>();
 }
 
 // decode: `enc` may live in HBM or in mapped pinned host memory (zero-copy
-// swap-in).  Each CTA walks its tiles with a two-deep pipeline: the bulk
-// load of tile k+1's chunk is in flight while tile k is expanded from shared
-// memory into coalesced HBM stores.
+// swap-in).  Each CTA walks its tiles with a two-deep pipeline: the bulk load
+// of tile k+1's chunk is in flight while tile k is expanded from shared memory
+// into coalesced HBM stores; tile entries are read one tile further ahead.
 __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict__ enc, uint64_t nwords,
                                                          uint32_t* __restrict__ dst, int use_bulk) {
-  extern __shared__ __align__(128) uint32_t zsm[];
+  extern __shared__ __align__(128) unsigned char zsm[];
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ uint32_t seg[kZvcMaskWords + 1];
-  __shared__ uint32_t s_mode;
-  const ZvcHeader* h = reinterpret_cast<const ZvcHeader*>(enc);
-  if (threadIdx.x == 0) s_mode = h->mode;
-  __syncthreads();
-  if (s_mode == 0) {
-    zvc_raw_copy(dst, reinterpret_cast<const uint32_t*>(enc + 64), nwords);
-    return;
-  }
+  __shared__ uint32_t s_info[2];
   const uint64_t ntiles = zvc_tiles(nwords);
-  const uint32_t* offs = reinterpret_cast<const uint32_t*>(enc + 64);
+  const ZvcTile* table = reinterpret_cast<const ZvcTile*>(enc + 64);
   const char* data = enc + zvc_data_pos(ntiles);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
   if (use_bulk) {
     if (threadIdx.x == 0) {
       mbar_init(&bar[0], 1);
@@ -566,20 +593,31 @@ __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict_
     }
     __syncthreads();
   }
-  auto issue = [&](uint64_t t, int b) {  // thread 0 only
-    const uint32_t a = offs[t], e = offs[t + 1];
-    const uint32_t bytes = (e - a) * 16;
+  ZvcTile next{0, 0};   // thread 0: the entry of the tile after the one in flight
+  auto issue = [&](uint64_t t, int b, uint32_t bytes) {  // thread 0 only
     mbar_expect_tx(&bar[b], bytes);
-    bulk_g2s(zsm + b * kZvcChunkWords, data + uint64_t(a) * 16, bytes, &bar[b]);
+    bulk_g2s(zsm + b * kZvcBufBytes, data + t * kZvcSlotBytes, bytes, &bar[b]);
   };
   uint32_t phase0 = 0, phase1 = 0;
-  if (use_bulk && threadIdx.x == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  if (threadIdx.x == 0 && blockIdx.x < ntiles) {
+    const ZvcTile e0 = table[blockIdx.x];
+    s_info[0] = e0.info;
+    if (use_bulk) issue(blockIdx.x, 0, e0.bytes);
+    if (blockIdx.x + gridDim.x < ntiles) next = table[blockIdx.x + gridDim.x];
+  }
   int b = 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, b ^= 1) {
-    uint32_t* chunk = zsm + b * kZvcChunkWords;
+    unsigned char* chunk = zsm + b * kZvcBufBytes;
+    const uint32_t* cw = reinterpret_cast<const uint32_t*>(chunk);
+    __syncthreads();   // s_info of this tile is published; buffer b^1 is free
+    const uint32_t info = s_info[b];
     if (use_bulk) {
       const uint64_t tn = t + gridDim.x;
-      if (threadIdx.x == 0 && tn < ntiles) issue(tn, b ^ 1);
+      if (threadIdx.x == 0 && tn < ntiles) {
+        s_info[b ^ 1] = next.info;
+        issue(tn, b ^ 1, next.bytes);
+        if (tn + gridDim.x < ntiles) next = table[tn + gridDim.x];
+      }
       if (b == 0) {
         mbar_wait(&bar[0], phase0);
         phase0 ^= 1;
@@ -588,26 +626,43 @@ __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict_
         phase1 ^= 1;
       }
     } else {
-      const uint32_t a = offs[t], e = offs[t + 1];
-      const uint4* s4 = reinterpret_cast<const uint4*>(data + uint64_t(a) * 16);
+      const ZvcTile e = table[t];
+      const uint4* s4 = reinterpret_cast<const uint4*>(data + t * kZvcSlotBytes);
       uint4* c4 = reinterpret_cast<uint4*>(chunk);
-      for (uint32_t k = threadIdx.x; k < e - a; k += 256) c4[k] = ld_stream(s4 + k);
+      for (uint32_t q = threadIdx.x; q < e.bytes / 16; q += 256) c4[q] = ld_stream(s4 + q);
+      if (threadIdx.x == 0 && t + gridDim.x < ntiles) s_info[b ^ 1] = table[t + gridDim.x].info;
       __syncthreads();
     }
-    if (threadIdx.x < kZvcMaskWords) seg[threadIdx.x] = __popc(chunk[threadIdx.x]);
-    __syncthreads();
-    if (warp == 0) zvc_seg_scan(seg, lane);
-    __syncthreads();
+    const uint32_t mode = info & 3u, k = (info >> 2) & 15u, sp = (info >> 6) & 1u, sc = (info >> 7) & 1u,
+                   em = (info >> 8) & 0x7Fu, n = info >> 16;
+    const bool masked = mode == kZMask || mode == kZExpM;
+    if (masked) {
+      if (threadIdx.x < kZvcMaskWords) seg[threadIdx.x] = __popc(cw[threadIdx.x]);
+      __syncthreads();
+      if (warp == 0) zvc_seg_scan(seg, lane);
+      __syncthreads();
+    }
+    const uint32_t hoff = mode == kZExpD ? zvc_pad16(3ull * n) : 512 + zvc_pad16(3ull * n);
+    const unsigned char* lo = chunk + (mode == kZExpM ? 512 : 0);
+    const uint32_t* hi = reinterpret_cast<const uint32_t*>(chunk + hoff);
     const uint64_t base = t * kZvcTileWords;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint64_t i = base + r * 256 + threadIdx.x;
-      const uint32_t m = chunk[r * 8 + warp];
-      const uint32_t v =
-          ((m >> lane) & 1u) ? chunk[kZvcMaskWords + seg[r * 8 + warp] + __popc(m & ((1u << lane) - 1u))] : 0u;
+      const uint32_t j = r * 256 + threadIdx.x;
+      const uint64_t i = base + j;
+      uint32_t v;
+      if (mode == kZRaw) {
+        v = cw[j < kZvcTileWords ? j : 0];
+      } else if (mode == kZExpD) {
+        v = i < nwords ? zvc_get_exp(lo, hi, j, k, sp, sc, em) : 0u;
+      } else {
+        const uint32_t m = cw[r * 8 + warp];
+        const uint32_t p = seg[r * 8 + warp] + __popc(m & lt);
+        v = ((m >> lane) & 1u) ? (mode == kZMask ? cw[kZvcMaskWords + p] : zvc_get_exp(lo, hi, p, k, sp, sc, em))
+                               : 0u;
+      }
       if (i < nwords) dst[i] = v;
     }
-    __syncthreads();  // chunk buffer b is free for the load issued two tiles from now
   }
 }
 

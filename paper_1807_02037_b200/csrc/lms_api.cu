@@ -202,10 +202,6 @@ struct lms_ctx {
   std::vector<lms_handle*> zombie;   // released handles waiting for H2D reads
   std::vector<lms_handle*> zvc_open; // ZVC swap-outs whose compressed size is not yet known
 
-  // ZVC scratch on the D2H stream
-  uint32_t* zvc_scratch = nullptr;
-  size_t zvc_scratch_words = 0;
-
   // stats
   lms_stats_t st{};
   int64_t next_id = 1;
@@ -662,7 +658,20 @@ int host_free_locked(lms_ctx* c, void* ptr) {
   return fail(LMS_E_INVALID, "lms_host_free: pointer not from the host pool");
 }
 
-// learn the compressed size of finished ZVC swap-outs (header in pinned memory)
+// bytes a finished encoded stream occupies on the wire: header + tile table +
+// each tile's chunk (host-readable stream; `bound` if it is not one)
+uint64_t zvc_wire_bytes(const char* enc, uint64_t bound) {
+  const ZvcHeader* hd = reinterpret_cast<const ZvcHeader*>(enc);
+  if (hd->magic != kZvcMagic) return bound;
+  const ZvcTile* tab = reinterpret_cast<const ZvcTile*>(enc + hd->table_pos);
+  uint64_t b = 64 + hd->ntiles * 8;
+  for (uint64_t t = 0; t < hd->ntiles; ++t) b += tab[t].bytes;
+  return b;
+}
+
+bool is_zvc(int codec) { return codec == LMS_CODEC_ZVC || codec == LMS_CODEC_ZX; }
+
+// learn the compressed size of finished ZVC swap-outs (table in pinned memory)
 void account_zvc(lms_ctx* c) {
   size_t w = 0;
   for (size_t i = 0; i < c->zvc_open.size(); ++i) {
@@ -671,8 +680,7 @@ void account_zvc(lms_ctx* c) {
       c->zvc_open[w++] = h;
       continue;
     }
-    const ZvcHeader* hd = reinterpret_cast<const ZvcHeader*>(h->host);
-    h->wire = hd->magic == kZvcMagic ? hd->bytes : h->host_bytes;
+    h->wire = zvc_wire_bytes(h->host, h->host_bytes);
     h->wire_known = true;
     c->st.d2h_wire_bytes += h->wire;
     c->st.h2d_wire_bytes += h->wire * h->zvc_in_pending;
@@ -1061,36 +1069,15 @@ bool is_host_ptr(const void* p) {
   return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
 }
 
-int ensure_zvc_scratch(lms_ctx* c, size_t words) {
-  if (words <= c->zvc_scratch_words) return LMS_OK;
-  if (c->zvc_scratch) {
-    CK(cudaStreamSynchronize(c->d2h));
-    cudaFree(c->zvc_scratch);
-    c->zvc_scratch = nullptr;
-  }
-  size_t w = std::max(words, size_t(1) << 16);
-  c->st.n_scratch_grow++;
-  CK(cudaMalloc(&c->zvc_scratch, w * 4));
-  c->zvc_scratch_words = w;
-  return LMS_OK;
-}
-
 int launch_zvc_encode(lms_ctx* c, const uint32_t* src, uint64_t nwords, char* out, cudaStream_t s,
-                      bool to_host) {
+                      bool to_host, bool allow_exp) {
   const uint64_t ntiles = zvc_tiles(nwords);
-  int rc = ensure_zvc_scratch(c, 2 * ntiles + 2);
-  if (rc) return rc;
-  uint32_t* counts = c->zvc_scratch;
-  uint32_t* offsets = c->zvc_scratch + ntiles;
-  // pass 1 reads HBM only: the whole GPU; pass 3 writes the host link (or
-  // HBM): enough CTAs to keep the link busy without crowding the compute stream
-  const int grid_count = sm_grid(c, int64_t(ntiles), 1);
-  int grid_enc = grid_count;
-  if (to_host) grid_enc = int(std::min<int64_t>(int64_t(ntiles), c->zc_ctas));
-  zvc_count_kernel<<<grid_count, 256, 0, s>>>(src, nwords, counts);
-  zvc_scan_kernel<<<1, 1024, 0, s>>>(counts, nwords, offsets, out);
-  zvc_encode_kernel<<<std::max(grid_enc, 1), 256, kZvcSmemBytes, s>>>(src, nwords, offsets, out, c->use_bulk);
-  c->st.kernel_launches += 3;
+  // one pass: HBM-side encodes take the whole GPU; encodes into pinned memory
+  // take enough CTAs to keep the link busy without crowding the compute stream
+  int grid = sm_grid(c, int64_t(ntiles), 1);
+  if (to_host) grid = int(std::min<int64_t>(int64_t(ntiles), c->zc_ctas));
+  zvc_encode_kernel<<<std::max(grid, 1), 256, kZvcSmemBytes, s>>>(src, nwords, out, c->use_bulk, allow_exp);
+  c->st.kernel_launches++;
   CK(cudaGetLastError());
   return LMS_OK;
 }
@@ -1248,7 +1235,6 @@ int lms_destroy(lms_ctx* c) {
     delete ch.arena;
   }
   delete c->vmm;
-  if (c->zvc_scratch) cudaFree(c->zvc_scratch);
   if (c->h2d && c->h2d != c->d2h) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   delete c;
@@ -1582,11 +1568,15 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
   h->logical = uint64_t(h->numel) * elem_size;
   const uint64_t stored = h->packed ? h->logical : uint64_t(h->span) * elem_size;
   const bool aligned = reinterpret_cast<uintptr_t>(src) % 16 == 0;
-  if (codec == LMS_CODEC_ZVC && (h->packed || stored % 4 != 0 || !aligned)) codec = LMS_CODEC_RAW_SM;
+  if (codec < LMS_CODEC_RAW_CE || codec > LMS_CODEC_ZX) {
+    delete h;
+    return fail(LMS_E_INVALID, "unknown codec");
+  }
+  if (is_zvc(codec) && (h->packed || stored % 4 != 0 || !aligned)) codec = LMS_CODEC_RAW_SM;
   if (codec == LMS_CODEC_RAW_SM && !h->packed && !aligned) codec = LMS_CODEC_RAW_CE;
   if (h->packed) codec = LMS_CODEC_RAW_SM;  // fused pack straight into pinned memory
   h->codec = codec;
-  h->host_bytes = codec == LMS_CODEC_ZVC ? zvc_bound(stored / 4) : (stored ? stored : 16);
+  h->host_bytes = is_zvc(codec) ? zvc_bound(stored / 4) : (stored ? stored : 16);
   int rc = host_alloc_locked(c, h->host_bytes, reinterpret_cast<void**>(&h->host));
   if (rc) {
     delete h;
@@ -1609,8 +1599,9 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
         rc = launch_copy(c, h->host, static_cast<const char*>(src), stored, s);
       h->wire = stored;
     } else {
-      rc = launch_zvc_encode(c, static_cast<const uint32_t*>(src), stored / 4, h->host, s, true);
-      h->wire = h->host_bytes;  // upper bound until the header is readable
+      rc = launch_zvc_encode(c, static_cast<const uint32_t*>(src), stored / 4, h->host, s, true,
+                             codec == LMS_CODEC_ZX);
+      h->wire = h->host_bytes;  // upper bound until the tile table is readable
     }
     if (rc) {
       host_free_locked(c, h->host);
@@ -1627,7 +1618,7 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
     h->rec_gen = c->trace_gen;
   }
   timing_end(c, s, t0, h, 0, h->logical, h->wire);
-  if (codec == LMS_CODEC_ZVC && stored) {
+  if (is_zvc(codec) && stored) {
     h->wire_known = false;
     c->zvc_open.push_back(h);
   }
@@ -1642,7 +1633,7 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
   c->st.n_swap_out++;
   c->st.n_handles_live++;
   c->st.d2h_logical_bytes += h->logical;
-  if (codec != LMS_CODEC_ZVC) c->st.d2h_wire_bytes += h->wire;
+  if (!is_zvc(codec)) c->st.d2h_wire_bytes += h->wire;
   *out = h;
   return LMS_OK;
 }
@@ -1683,12 +1674,12 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
   if (stored) {
     if (!natural) {
       // arbitrary destination layout: scatter straight out of pinned memory
-      if (h->codec == LMS_CODEC_ZVC) return fail(LMS_E_INVALID, "ZVC handles restore to their own layout");
+      if (is_zvc(h->codec)) return fail(LMS_E_INVALID, "ZVC handles restore to their own layout");
       if (!h->packed)
         return fail(LMS_E_INVALID, "a dense view restores only into its own strides (pass NULL)");
       rc = launch_layout<false>(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
       wire = stored;
-    } else if (h->codec == LMS_CODEC_ZVC) {
+    } else if (is_zvc(h->codec)) {
       // zero-copy: the decode kernel reads the compressed stream straight out
       // of pinned memory, so only the compressed bytes cross the link and no
       // device staging buffer is taken from the budget
@@ -1707,7 +1698,7 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
   CK(cudaEventRecord(h->in_ready, s));
   if (c->cfg.timing && t0) {
     h->rec_in = int64_t(c->recs.size());
-    if (h->codec == LMS_CODEC_ZVC && !h->wire_known) {
+    if (is_zvc(h->codec) && !h->wire_known) {
       if (h->rec_gen != c->trace_gen) h->zvc_in_recs.clear();
       h->zvc_in_recs.push_back(h->rec_in);
     }
@@ -1716,7 +1707,7 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
   timing_end(c, s, t0, h, 1, h->logical, wire);
   c->st.n_swap_in++;
   c->st.h2d_logical_bytes += h->logical;
-  if (h->codec == LMS_CODEC_ZVC && !h->wire_known)
+  if (is_zvc(h->codec) && !h->wire_known)
     h->zvc_in_pending++;  // counted when the swap-out's header is readable
   else
     c->st.h2d_wire_bytes += wire;
@@ -1754,10 +1745,7 @@ int lms_handle_release(lms_ctx* c, lms_handle* h) {
 
 int lms_handle_info(lms_handle* h, int64_t* id, uint64_t* logical, uint64_t* wire, int* codec) {
   if (!h) return fail(LMS_E_INVALID, "null handle");
-  if (!h->wire_known && cudaEventQuery(h->out_done->e) == cudaSuccess) {
-    const ZvcHeader* hd = reinterpret_cast<const ZvcHeader*>(h->host);
-    if (hd->magic == kZvcMagic) h->wire = hd->bytes;
-  }
+  if (!h->wire_known && cudaEventQuery(h->out_done->e) == cudaSuccess) h->wire = zvc_wire_bytes(h->host, h->host_bytes);
   if (id) *id = h->id;
   if (logical) *logical = h->logical;
   if (wire) *wire = h->wire;
@@ -1808,13 +1796,13 @@ int lms_unpack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, con
 
 size_t lms_zvc_bound(size_t nwords) { return zvc_bound(nwords); }
 
-int lms_zvc_encode(lms_ctx* c, const void* src, size_t nwords, void* dst, void* stream) {
+int lms_zvc_encode(lms_ctx* c, const void* src, size_t nwords, void* dst, int exponents, void* stream) {
   if (!c || (!src && nwords) || !dst) return fail(LMS_E_INVALID, "null argument");
   if (reinterpret_cast<uintptr_t>(src) % 16 || reinterpret_cast<uintptr_t>(dst) % 16)
     return fail(LMS_E_INVALID, "zvc buffers must be 16-byte aligned");
   std::lock_guard<std::mutex> g(c->mu);
   return launch_zvc_encode(c, static_cast<const uint32_t*>(src), nwords, static_cast<char*>(dst),
-                           static_cast<cudaStream_t>(stream), is_host_ptr(dst));
+                           static_cast<cudaStream_t>(stream), is_host_ptr(dst), exponents != 0);
 }
 
 int lms_zvc_decode(lms_ctx* c, const void* enc, size_t nwords, void* dst, void* stream) {
@@ -1864,7 +1852,7 @@ int lms_zvc_encoded_size(const void* enc_host, size_t* out) {
   if (!enc_host || !out) return fail(LMS_E_INVALID, "null argument");
   const ZvcHeader* h = static_cast<const ZvcHeader*>(enc_host);
   if (h->magic != kZvcMagic) return fail(LMS_E_INVALID, "not a ZVC stream");
-  *out = h->bytes;
+  *out = zvc_wire_bytes(static_cast<const char*>(enc_host), 0);
   return LMS_OK;
 }
 

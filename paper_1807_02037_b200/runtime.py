@@ -18,8 +18,8 @@ LIB_PATH = os.path.join(_HERE, "liblms.so")
 SHIM_PATH = os.path.join(_HERE, "liblms_torch.so")   # PyTorch allocator hooks (throw c10 OOM)
 
 LMS_OK, LMS_E_INVALID, LMS_E_OOM, LMS_E_HOST_OOM, LMS_E_CUDA, LMS_E_STATE = 0, -1, -2, -3, -4, -5
-CODEC_RAW_CE, CODEC_RAW_SM, CODEC_ZVC = 0, 1, 2
-CODECS = {"ce": CODEC_RAW_CE, "sm": CODEC_RAW_SM, "zvc": CODEC_ZVC}
+CODEC_RAW_CE, CODEC_RAW_SM, CODEC_ZVC, CODEC_ZX = 0, 1, 2, 3
+CODECS = {"ce": CODEC_RAW_CE, "sm": CODEC_RAW_SM, "zvc": CODEC_ZVC, "zx": CODEC_ZX}
 MAX_DIMS = 8
 
 
@@ -113,7 +113,7 @@ def lib():
         "lms_handle_layout": ([vp, i64p, i64p], i),
         "lms_pack": ([vp, vp, vp, i64p, i64p, i, i, vp], i),
         "lms_unpack": ([vp, vp, vp, i64p, i64p, i, i, vp], i),
-        "lms_zvc_bound": ([sz], sz), "lms_zvc_encode": ([vp, vp, sz, vp, vp], i),
+        "lms_zvc_bound": ([sz], sz), "lms_zvc_encode": ([vp, vp, sz, vp, i, vp], i),
         "lms_zvc_decode": ([vp, vp, sz, vp, vp], i),
         "lms_zvc_encoded_size": ([vp, ctypes.POINTER(sz)], i),
         "lms_stats": ([vp, ctypes.POINTER(_Stats)], i),
@@ -369,9 +369,18 @@ class Context:
     def zvc_bound(self, nwords: int) -> int:
         return lib().lms_zvc_bound(nwords)
 
-    def zvc_encode(self, src, dst, stream=None):
+    def zvc_encode(self, src, dst, stream=None, exponents: bool = False):
+        """One-pass encode of ``src``'s 32-bit words into ``dst`` (ZVC v3;
+        ``exponents``: the ZX tile forms are allowed too)."""
         _check(lib().lms_zvc_encode(self.ptr, src.data_ptr(), src.numel() * src.element_size() // 4,
-                                    dst.data_ptr(), _stream_ptr(stream)), "lms_zvc_encode")
+                                    dst.data_ptr(), int(exponents), _stream_ptr(stream)), "lms_zvc_encode")
+
+    @staticmethod
+    def zvc_encoded_size(enc_host) -> int:
+        """Wire bytes of an encoded stream held in host memory (a CPU uint8 tensor)."""
+        n = ctypes.c_size_t()
+        _check(lib().lms_zvc_encoded_size(enc_host.data_ptr(), ctypes.byref(n)), "lms_zvc_encoded_size")
+        return n.value
 
     def zvc_decode(self, enc, dst, stream=None):
         _check(lib().lms_zvc_decode(self.ptr, enc.data_ptr(), dst.numel() * dst.element_size() // 4,

@@ -655,6 +655,7 @@ class _ForwardSwaps(TorchFunctionMode):
                             self._swap_in(x)
                         self.ctx.wait(x["h"], torch.cuda.current_stream())
                         x["phase"] = "restored"
+                        x["t"] = None     # the model's own references decide its lifetime again
                         del self.freed[x["key"]]
         out = func(*args, **kwargs)
         seen = set()
@@ -677,7 +678,11 @@ class _ForwardSwaps(TorchFunctionMode):
                 self._swap_in(x)
             self.ctx.wait(x["h"], torch.cuda.current_stream())
             x["phase"] = "restored"
+            x["t"] = None
         self.freed.clear()
+        # tensors swapped out but never freed (no release point reached) are not pinned either
+        for x in self.state.values():
+            x.pop("t", None)
 
 
 class _SwapRef:

@@ -79,11 +79,12 @@ def test_unpack_matches_copy(lms_ctx, dtype, tma):
     lms_ctx.set_tuning(0, -1, 1)
 
 
+@pytest.mark.parametrize("exponents", [0, 1])
 @pytest.mark.parametrize("bulk", [1, 0])
 @pytest.mark.parametrize("nwords,density", [(0, 0.5), (1, 1.0), (3, 0.0), (4095, 0.5), (4096, 0.5),
                                             (4097, 0.3), (1 << 20, 0.5), (1 << 20, 0.0),
                                             (1 << 20, 1.0), ((1 << 22) + 13, 0.47)])
-def test_zvc_roundtrip(lms_ctx, nwords, density, bulk):
+def test_zvc_roundtrip(lms_ctx, nwords, density, bulk, exponents):
     lms_ctx.set_tuning(0, bulk)
     torch.manual_seed(nwords)
     x = torch.randn(nwords, device="cuda")
@@ -93,13 +94,71 @@ def test_zvc_roundtrip(lms_ctx, nwords, density, bulk):
         x[7] = float("nan")
     bound = lms_ctx.zvc_bound(nwords)
     enc = torch.empty(max(bound, 16), dtype=torch.uint8, device="cuda")
-    lms_ctx.zvc_encode(x, enc)
+    lms_ctx.zvc_encode(x, enc, exponents=bool(exponents))
     out = torch.full_like(x, 7.0)
     lms_ctx.zvc_decode(enc, out)
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int32), x.view(torch.int32))
-    hdr = enc[:64].cpu().view(torch.int64)
-    nnz = int((x.view(torch.int32) != 0).sum())
     if nwords:
-        assert int(hdr[3]) == nnz  # total_nnz field
+        host = enc.cpu()
+        hdr = host[:64].view(torch.int64)
+        assert int(hdr[1]) == nwords and int(hdr[2]) == (nwords + 4095) // 4096
+        wire = lms_ctx.zvc_encoded_size(host)
+        assert wire <= bound
+        if density == 0.0:
+            assert wire <= 64 + 8 * int(hdr[2]) + 512 * int(hdr[2])
     lms_ctx.set_tuning(0, 1)
+
+
+def _special_words(n, g):
+    """fp32 bit patterns the exponent planes must carry exactly."""
+    x = torch.randn(n, device="cuda", generator=g)
+    specials = torch.tensor([0.0, -0.0, float("inf"), float("-inf"), float("nan"), 1e-45, -1e-45, 1e-38,
+                             3.4e38, -3.4e38, 1.0, -1.0], device="cuda")
+    idx = torch.randint(0, n, (min(n, 64),), device="cuda", generator=g)
+    x[idx] = specials[torch.arange(idx.numel(), device="cuda") % specials.numel()]
+    return x
+
+
+@pytest.mark.parametrize("n", [5, 4096, 4096 * 7 + 11, 1 << 22])
+def test_zx_exponent_planes_roundtrip(lms_ctx, n):
+    """ZX tiles (exponent planes over all words or over the nonzero ones): bit-exact
+    on normal activations, all-positive ReLU outputs (no sign plane), scaled
+    ranges (wide exponent bands) and special values."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    cases = {
+        "normal": torch.randn(n, device="cuda", generator=g),
+        "relu": torch.relu(torch.randn(n, device="cuda", generator=g)),
+        "wide": torch.randn(n, device="cuda", generator=g) * torch.exp(8 * torch.randn(n, device="cuda", generator=g)),
+        "special": _special_words(n, g),
+        "ints": torch.randint(-2**31, 2**31 - 1, (n,), device="cuda", dtype=torch.int32, generator=g).view(torch.float32),
+    }
+    for name, x in cases.items():
+        enc = torch.empty(lms_ctx.zvc_bound(n), dtype=torch.uint8, device="cuda")
+        lms_ctx.zvc_encode(x, enc, exponents=True)
+        out = torch.empty_like(x)
+        lms_ctx.zvc_decode(enc, out)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int32), x.view(torch.int32)), name
+        if n >= 4096 and name in ("normal", "relu"):
+            wire = lms_ctx.zvc_encoded_size(enc.cpu())
+            # normal: sign + ~3-4 exponent bits + 24 low bits per word; relu: mask + no sign
+            assert wire < (0.92 if name == "normal" else 0.5) * 4 * n, (name, wire / (4 * n))
+
+
+def test_zx_swap_roundtrip_and_wire(lms_ctx):
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(64, 256, 28, 28, device="cuda", generator=g)
+    for codec in ("zx", "zvc"):
+        h = lms_ctx.swap_out(x, codec)
+        out = lms_ctx.swap_in(h)
+        lms_ctx.wait(h)
+        torch.cuda.synchronize()
+        lms_ctx.synchronize()
+        wire = lms_ctx.wire_bytes(h)
+        lms_ctx.release(h)
+        assert torch.equal(out, x), codec
+        if codec == "zx":
+            assert wire < 0.92 * x.numel() * 4
+        else:
+            assert wire >= x.numel() * 4   # dense: ZVC keeps raw tiles

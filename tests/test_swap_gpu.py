@@ -49,7 +49,8 @@ def test_zvc_shrinks_sparse_and_not_dense(lms_ctx):
     torch.cuda.synchronize()
     lms_ctx.synchronize()
     assert lms_ctx.wire_bytes(hs) < 0.6 * sparse.numel() * 4
-    assert lms_ctx.wire_bytes(hd) <= dense.numel() * 4 + 64  # raw fallback, never bigger
+    # raw tiles: never bigger than the words plus the header and the tile table
+    assert lms_ctx.wire_bytes(hd) <= dense.numel() * 4 + 64 + 8 * (dense.numel() // 4096)
     for h in (hs, hd):
         out = lms_ctx.swap_in(h)
         lms_ctx.wait(h)
@@ -99,7 +100,7 @@ def test_stats_count_bytes_and_kernels(lms_ctx):
     lms_ctx.synchronize()
     st = lms_ctx.stats()
     assert st["d2h_logical_bytes"] == 4 << 20 and st["h2d_logical_bytes"] == 4 << 20
-    assert st["kernel_launches"] >= 4  # count, scan, encode, decode
+    assert st["kernel_launches"] >= 2  # one-pass encode, decode
     assert 0 < st["d2h_wire_bytes"] < 4 << 20
     tr = lms_ctx.trace()
     assert {r["direction"] for r in tr} == {0, 1}
