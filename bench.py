@@ -49,7 +49,10 @@ def parse():
     ap.add_argument("--budget-gib", type=float, default=16.0)
     ap.add_argument("--factor", type=float, default=4.7)
     ap.add_argument("--batch", type=int, default=0, help="swapped batch (default: factor x B0)")
-    ap.add_argument("--codec", default="auto", choices=["ce", "sm", "zvc", "auto"])
+    ap.add_argument("--codec", default="auto", choices=["ce", "sm", "zvc", "zx", "auto"])
+    ap.add_argument("--zx-max-ratio", type=float, default=0.0,
+                    help="auto codec: ZX for tensors whose capture-time ZX ratio is at most this "
+                         "(0 = SwapExecutor.ZX_MAX_RATIO)")
     ap.add_argument("--lb", type=int, default=1)
     ap.add_argument("--ub", type=int, default=10000)
     ap.add_argument("--strategy", default="chain_rule")
@@ -229,10 +232,6 @@ def main():
     gc.collect()
     use_dist = ws > 1 or args.ddp
     if use_dist:
-        # tuning runs a rank-local, timing-dependent number of steps: under DDP
-        # every rank must step together, so replicas keep the rewrite's windows
-        args.tune_windows = 0
-    if use_dist:
         import torch.distributed as dist
         for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511"), ("RANK", "0"), ("WORLD_SIZE", "1")):
             os.environ.setdefault(k, v)
@@ -304,6 +303,13 @@ def main():
         model = torch.nn.parallel.DistributedDataParallel(base_model, device_ids=[local])
         if lms is not None:
             lms.model = model
+
+    def tune_agree(v, op):
+        """The tuner's decisions common to every DDP rank (None without DDP)."""
+        return agree(v, op)
+
+    if not use_dist:
+        tune_agree = None   # noqa: F811
 
     def agree(v, op="min"):
         if ws == 1:
@@ -387,6 +393,9 @@ def main():
                          fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance)
     codec = args.codec
     # tensors under 64 KiB at the capture size stay on the device
+    if args.zx_max_ratio > 0:
+        from paper_1807_02037_b200.torch_lms import SwapExecutor
+        SwapExecutor.ZX_MAX_RATIO = args.zx_max_ratio
     lms = LMS(model, loss_fn, opt, cfg0, ctx, codec=codec, min_swap_bytes=64 << 10)
     t_cap = time.perf_counter()
     plan = lms.capture(xc, yc)
@@ -532,10 +541,14 @@ def main():
             if tune and prepared is not None:
                 lms.cfg = prepared[0]
                 lms._set_plan(prepared[1])
-                tuned = dict(prepared[2], reused=True)
+                # record the chosen plan once more and time it: the timed run then
+                # replays exactly this recorded placement
+                final = lms._timed_replay(xs, ys, 5, tune_agree)
+                tuned = dict(prepared[2], reused=True, final_ms=final["ms"] if final else None,
+                             final_spread_ms=final["spread"] if final else None)
                 prepared = None     # a retry (OOM) tunes afresh
             elif tune:
-                tuned = lms.tune_windows(xs, ys)
+                tuned = lms.tune_windows(xs, ys, agree=tune_agree)
                 log(f"[bench] tune_windows: {tuned}")
             for _ in range(args.warmup):
                 lms.step(xs, ys)
@@ -600,7 +613,7 @@ def main():
         joint, joint_plan = {}, {}
         t_joint = time.perf_counter()
         for n in cands:
-            if time.perf_counter() - t_joint > args.tune_budget_s:
+            if agree(time.perf_counter() - t_joint, "max") > args.tune_budget_s:
                 log(f"[bench] joint search budget spent; skipping n_tensors={n}")
                 break
             lms.replan(RewriteConfig(n_tensors=n if n < N else -1, lb=args.lb, ub=args.ub,
@@ -608,9 +621,9 @@ def main():
                                  branch_threshold=args.branch_threshold, fuse_swapins=args.fuse_swapins,
                                      swapin_fuse_distance=args.fuse_distance))
             try:
-                info = lms.tune_windows(xs, ys)
+                info = lms.tune_windows(xs, ys, agree=tune_agree)
             except RuntimeError as e:
-                if not is_oom(e):
+                if not is_oom(e) or use_dist:
                     raise
                 traceback.clear_frames(e.__traceback__)
                 info = {}
@@ -708,7 +721,7 @@ def main():
     # per transfer path: wire bytes over the summed spans of its transfers
     # (CUDA events on the copy channel each transfer ran on)
     paths = {}
-    names = {0: "copy-engine", 1: "sm-zero-copy", 2: "zvc-zero-copy"}
+    names = {0: "copy-engine", 1: "sm-zero-copy", 2: "zvc-zero-copy", 3: "zx-zero-copy"}
     for r in trace:
         key = f"{'d2h' if r['direction'] == 0 else 'h2d'}:{names.get(r['codec'], r['codec'])}"
         p = paths.setdefault(key, {"bytes": 0, "logical": 0, "ms": 0.0, "n": 0})
@@ -730,7 +743,7 @@ def main():
         dom_peak = link.get(dom_key.split(":")[0]) if link else None
         achieved = paths[dom_key]["wire_gbs"]
         roof = {"bound": "host-link", "kernel": dom_key + (" (zvc_encode_kernel/zvc_decode_kernel)"
-                                                          if "zvc" in dom_key else ""),
+                                                          if ("zvc" in dom_key or "zx" in dom_key) else ""),
                 "achieved": achieved, "peak": round(dom_peak, 2) if dom_peak else None, "unit": "GB/s",
                 "frac": round(achieved / dom_peak, 4) if dom_peak else None, "traffic": None,
                 "peak_source": "pinned copy-engine copy of 512 MiB measured in this run (host link has no "

@@ -96,6 +96,8 @@ typedef struct {
   uint64_t n_host_grow;    /* pinned chunks added */
   uint64_t n_scratch_grow; /* always 0 (the one-pass ZVC v3 codec has no scratch); kept for the ABI */
   double unmap_ms, map_ms, access_ms;  /* pool_driver_ms split by driver call */
+  int64_t numa_node;              /* the GPU's NUMA node pinned chunks are placed on (-1: none) */
+  uint64_t n_host_chunks_on_node; /* pinned chunks whose pages landed on that node */
 } lms_stats_t;
 
 /* one measured transfer, in the TraceEvent vocabulary (sim.py:74-81) */

@@ -323,6 +323,7 @@ constexpr int kZvcMaskWords = kZvcTileWords / 32;                 // 128
 constexpr uint32_t kZvcSlotBytes = kZvcTileWords * 4;             // 16 KiB
 constexpr int kZvcBufBytes = kZvcSlotBytes + 512;                 // chunk buffer (+ scratch slack)
 constexpr int kZvcSmemBytes = 2 * kZvcBufBytes;                   // double-buffered
+constexpr int kZvcEncSmemBytes = kZvcSmemBytes + 2 * kZvcSlotBytes;  // + two prefetched input tiles
 constexpr uint32_t kZvcMagic = 0x3343565Au;                       // "ZVC3"
 enum { kZRaw = 0, kZMask = 1, kZExpD = 2, kZExpM = 3 };
 
@@ -425,6 +426,29 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
   char* data = out + dpos;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
+  // input tiles are prefetched one ahead by bulk copies (HBM -> shared) so a
+  // CTA's loads overlap its previous tile's encode and store
+  __shared__ __align__(8) uint64_t ibar[2];
+  const bool pref = use_bulk && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  const uint32_t* inbuf = reinterpret_cast<const uint32_t*>(zsm + kZvcSmemBytes);
+  auto load_tile = [&](uint64_t tt, int b) {   // thread 0 only
+    const uint64_t tb = tt * kZvcTileWords;
+    const uint32_t nv = uint32_t(nwords - tb < kZvcTileWords ? nwords - tb : kZvcTileWords);
+    const uint32_t bytes = (nv * 4) & ~15u;
+    fence_proxy_async_smem();   // earlier generic reads of this buffer come first
+    mbar_expect_tx(&ibar[b], bytes);
+    if (bytes) bulk_g2s(zsm + kZvcSmemBytes + b * kZvcSlotBytes, src + tb, bytes, &ibar[b]);
+  };
+  if (pref) {
+    if (threadIdx.x == 0) {
+      mbar_init(&ibar[0], 1);
+      mbar_init(&ibar[1], 1);
+      fence_mbar_init();
+      if (blockIdx.x < ntiles) load_tile(blockIdx.x, 0);
+    }
+    __syncthreads();
+  }
+  uint32_t iph0 = 0, iph1 = 0;
   int buf = 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
     unsigned char* chunk = zsm + buf * kZvcBufBytes;
@@ -434,10 +458,28 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
     const uint64_t base = t * kZvcTileWords;
     const uint32_t nvalid = uint32_t(nwords - base < kZvcTileWords ? nwords - base : kZvcTileWords);
     uint32_t w16[16];
+    if (pref) {
+      if (threadIdx.x == 0 && t + gridDim.x < ntiles) load_tile(t + gridDim.x, buf ^ 1);
+      if (buf == 0) {
+        mbar_wait(&ibar[0], iph0);
+        iph0 ^= 1;
+      } else {
+        mbar_wait(&ibar[1], iph1);
+        iph1 ^= 1;
+      }
+      const uint32_t* win = inbuf + buf * kZvcTileWords;
+      const uint32_t nbulk = (nvalid * 4 & ~15u) / 4;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const uint64_t i = base + r * 256 + threadIdx.x;
-      w16[r] = i < nwords ? __ldg(src + i) : 0u;
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t j = r * 256 + threadIdx.x;
+        w16[r] = j < nbulk ? win[j] : (j < nvalid ? __ldg(src + base + j) : 0u);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint64_t i = base + r * 256 + threadIdx.x;
+        w16[r] = i < nwords ? __ldg(src + i) : 0u;
+      }
     }
     // per-tile statistics: nonzeros, and the top-byte ranges over all / nonzero words
     uint32_t nnz = 0, mn_a = 127, mx_a = 0, or_a = 0, and_a = 1, mn_z = 127, mx_z = 0, or_z = 0, and_z = 1;

@@ -29,6 +29,10 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include "../../include/lms.h"
 #include "arena.h"
 #include "kernels.cuh"
@@ -53,6 +57,56 @@ static int fail(int code, const std::string& msg) {
   } while (0)
 
 static void* const kFresh = reinterpret_cast<void*>(~uintptr_t(0));
+
+// NVTX ranges on the host side of every swap/pool call (no-ops unless a tool
+// such as nsys is attached): the timeline shows when each transfer was issued
+// and where allocations waited for swap-out copies
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// ---------------------------------------------------------------------------
+// NUMA: pinned host chunks are placed on the GPU's own NUMA node (its PCIe
+// root complex), so each DP rank's swap traffic stays on its socket's memory
+// controllers.  Raw syscalls: libnuma is not a dependency.
+
+int device_numa_node(int device) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  for (char* q = bus; *q; ++q) *q = char(tolower(*q));
+  std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  FILE* f = fopen(path.c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node;
+}
+
+// prefer `node` for the pages this thread faults in while in scope
+struct NumaPrefer {
+  bool on = false;
+  explicit NumaPrefer(int node) {
+    if (node < 0 || node >= 64) return;
+    unsigned long mask = 1ul << node;
+    on = syscall(SYS_set_mempolicy, 1 /* MPOL_PREFERRED */, &mask, 64) == 0;
+  }
+  ~NumaPrefer() {
+    if (on) syscall(SYS_set_mempolicy, 0 /* MPOL_DEFAULT */, nullptr, 0);
+  }
+};
+
+// NUMA node holding the page at p (-1 if unknown)
+int page_node(const void* p) {
+  int node = -1;
+  if (syscall(SYS_get_mempolicy, &node, nullptr, 0, const_cast<void*>(p), 3 /* MPOL_F_NODE|MPOL_F_ADDR */) != 0)
+    return -1;
+  return node;
+}
 
 struct OomError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -199,6 +253,8 @@ struct lms_ctx {
   std::vector<Chunk> chunks;
   size_t host_reserved = 0;
   size_t host_used = 0, host_peak = 0;
+  int numa_node = -1;                // the GPU's NUMA node (pinned chunks prefer it)
+  uint64_t chunks_on_node = 0;       // pinned chunks whose pages landed there
   std::vector<lms_handle*> zombie;   // released handles waiting for H2D reads
   std::vector<lms_handle*> zvc_open; // ZVC swap-outs whose compressed size is not yet known
 
@@ -213,6 +269,11 @@ struct lms_ctx {
   int use_bulk = 1;         // ZVC kernels move chunks with cp.async.bulk (LMS_ZVC_BULK=0: STG/LDG)
   int zc_ctas = 0;          // CTAs of the zero-copy (host-side) kernels
   int use_tma_pack = 1;     // pack/unpack of rows layouts through tensor maps (LMS_TMA_PACK=0: SIMT)
+  // strided (non-dense) swaps: packed/unpacked in HBM by the TMA kernels through a
+  // staging block owned by each copy channel, moved by the copy engine
+  // (LMS_STAGE_STRIDED=0: SIMT kernels straight to/from pinned memory)
+  int stage_strided = 1;
+  char* stage[2] = {nullptr, nullptr};   // [0] D2H channel, [1] H2D channel
   // consumer reached its wait (event on the consumer stream) vs swap-in record
   std::vector<std::pair<cudaEvent_t, int64_t>> waits;
 };
@@ -290,6 +351,7 @@ template <class F>
 void reap_until(lms_ctx* c, F enough) {
   reap_deferred(c, false);
   if (c->deferred.empty() || enough()) return;
+  NvtxRange nv("lms:alloc_wait_swap_out");
   const auto t0 = std::chrono::steady_clock::now();
   while (!c->deferred.empty() && !enough()) {
     auto it = c->holds.find(c->deferred.front().base);
@@ -627,7 +689,12 @@ int host_alloc_locked(lms_ctx* c, size_t size, void** out) {
   }
   void* p = nullptr;
   const auto t0 = std::chrono::steady_clock::now();
-  cudaError_t e = cudaHostAlloc(&p, grow, cudaHostAllocPortable | cudaHostAllocMapped);
+  cudaError_t e;
+  {
+    NumaPrefer np(c->numa_node);
+    e = cudaHostAlloc(&p, grow, cudaHostAllocPortable | cudaHostAllocMapped);
+  }
+  if (e == cudaSuccess && c->numa_node >= 0 && page_node(p) == c->numa_node) c->chunks_on_node++;
   c->st.host_grow_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   c->st.n_host_grow++;
   if (e != cudaSuccess) {
@@ -1044,6 +1111,85 @@ int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_
   return LMS_OK;
 }
 
+constexpr size_t kStageBytes = size_t(32) << 20;
+
+// the channel's staging block (allocated once from the pool, owned by that
+// stream: stream order alone keeps chunk k+1's pack behind chunk k's copy)
+char* stage_block(lms_ctx* c, int dir) {
+  cudaStream_t s = dir == 0 ? c->d2h : c->h2d;
+  if (dir == 1 && c->h2d == c->d2h) dir = 0;   // one shared channel: one block
+  if (!c->stage[dir]) {
+    if (!c->vmm) return nullptr;   // a context without a device pool does not grow one for this
+    void* p = nullptr;
+    const std::string keep = g_err;
+    // a one-off allocation: not part of any recorded or replayed step plan
+    const int mode = c->plan.mode;
+    c->plan.mode = LMS_PLAN_OFF;
+    const int rc = dev_alloc_locked(c, kStageBytes, s, &p);
+    c->plan.mode = mode;
+    if (rc != LMS_OK) {
+      g_err = keep;
+      return nullptr;   // no room: the SIMT zero-copy path serves this swap
+    }
+    c->stage[dir] = static_cast<char*>(p);
+  }
+  return c->stage[dir];
+}
+
+// dims before the first one longer than 1 are trivial: slabs along it are
+// contiguous ranges of the packed layout
+bool slab_dim(int ndim, const int64_t* sizes, int elem, int* k0, uint64_t* row_bytes) {
+  int k = 0;
+  while (k < ndim - 1 && sizes[k] == 1) ++k;
+  uint64_t rb = uint64_t(elem);
+  for (int j = k + 1; j < ndim; ++j) rb *= uint64_t(sizes[j]);
+  *k0 = k;
+  *row_bytes = rb;
+  return ndim > 0 && rb <= kStageBytes;
+}
+
+// strided swap-out: TMA pack of slabs into the D2H staging block + copy-engine
+// D2H of each.  Returns 1 (nothing enqueued) when staging cannot serve it.
+int staged_pack_d2h(lms_ctx* c, char* host, const char* src, int ndim, const int64_t* sizes,
+                    const int64_t* strides, int elem, cudaStream_t s) {
+  int k0;
+  uint64_t row;
+  if (!c->stage_strided || !slab_dim(ndim, sizes, elem, &k0, &row)) return 1;
+  char* stg = stage_block(c, 0);
+  if (!stg) return 1;
+  const int64_t per = int64_t(kStageBytes / row);
+  int64_t sz[LMS_MAX_DIMS];
+  std::memcpy(sz, sizes, sizeof(int64_t) * ndim);
+  for (int64_t a = 0; a < sizes[k0]; a += per) {
+    sz[k0] = std::min(per, sizes[k0] - a);
+    int rc = launch_layout<true>(c, stg, src + a * strides[k0] * elem, ndim, sz, strides, elem, s);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(host + a * row, stg, uint64_t(sz[k0]) * row, cudaMemcpyDeviceToHost, s));
+  }
+  return 0;
+}
+
+// strided swap-in into `dst` (layout dst_strides): copy-engine H2D of slabs of
+// the packed host copy into the H2D staging block + TMA unpack of each
+int staged_unpack_h2d(lms_ctx* c, char* dst, const char* host, int ndim, const int64_t* sizes,
+                      const int64_t* dst_strides, int elem, cudaStream_t s) {
+  int k0;
+  uint64_t row;
+  if (!c->stage_strided || !slab_dim(ndim, sizes, elem, &k0, &row)) return 1;
+  char* stg = stage_block(c, 1);
+  if (!stg) return 1;
+  const int64_t per = int64_t(kStageBytes / row);
+  int64_t sz[LMS_MAX_DIMS];
+  std::memcpy(sz, sizes, sizeof(int64_t) * ndim);
+  for (int64_t a = 0; a < sizes[k0]; a += per) {
+    sz[k0] = std::min(per, sizes[k0] - a);
+    CK(cudaMemcpyAsync(stg, host + a * row, uint64_t(sz[k0]) * row, cudaMemcpyHostToDevice, s));
+    int rc = launch_layout<false>(c, dst + a * dst_strides[k0] * elem, stg, ndim, sz, dst_strides, elem, s);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
 int launch_copy(lms_ctx* c, char* dst, const char* src, size_t bytes, cudaStream_t s) {
   size_t n16 = bytes / 16;
   if (n16) {
@@ -1076,7 +1222,7 @@ int launch_zvc_encode(lms_ctx* c, const uint32_t* src, uint64_t nwords, char* ou
   // take enough CTAs to keep the link busy without crowding the compute stream
   int grid = sm_grid(c, int64_t(ntiles), 1);
   if (to_host) grid = int(std::min<int64_t>(int64_t(ntiles), c->zc_ctas));
-  zvc_encode_kernel<<<std::max(grid, 1), 256, kZvcSmemBytes, s>>>(src, nwords, out, c->use_bulk, allow_exp);
+  zvc_encode_kernel<<<std::max(grid, 1), 256, kZvcEncSmemBytes, s>>>(src, nwords, out, c->use_bulk, allow_exp);
   c->st.kernel_launches++;
   CK(cudaGetLastError());
   return LMS_OK;
@@ -1167,12 +1313,17 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
     return fail(LMS_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  c->numa_node = device_numa_node(c->device);
+  if (const char* v = getenv("LMS_NUMA")) {
+    if (atoi(v) < 0) c->numa_node = -1;   // LMS_NUMA=-1: no placement policy
+  }
   // zero-copy kernels: one CTA per SM by default (each keeps a 16 KiB chunk
   // in flight on the link), overridable for tuning
   c->zc_ctas = cfg->sm_ctas > 0 ? cfg->sm_ctas : c->num_sms;
   if (const char* v = getenv("LMS_ZC_CTAS")) c->zc_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("LMS_ZVC_BULK")) c->use_bulk = atoi(v) != 0;
   if (const char* v = getenv("LMS_TMA_PACK")) c->use_tma_pack = atoi(v) != 0;
+  if (const char* v = getenv("LMS_STAGE_STRIDED")) c->stage_strided = atoi(v) != 0;
   cudaFuncSetAttribute(tma_copy_kernel<kTmaStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kTmaStages * int(kTmaBoxTarget) * 2);
   cudaFuncSetAttribute(tma_transpose_kernel<1, tt_warps<1>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1183,7 +1334,7 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
                        int(tma_transpose_smem<4>()));
   cudaFuncSetAttribute(tma_transpose_kernel<8, tt_warps<8>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(tma_transpose_smem<8>()));
-  cudaFuncSetAttribute(zvc_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
+  cudaFuncSetAttribute(zvc_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcEncSmemBytes);
   cudaFuncSetAttribute(zvc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1381,6 +1532,7 @@ int lms_plan_end(lms_ctx* c) {
     return LMS_OK;
   }
   if (mode != LMS_PLAN_RECORD) return LMS_OK;
+  NvtxRange nv("lms:plan_place");
   P.rec_live.clear();  // still live at the end: t1 < 0, served dynamically
   P.rec_held.clear();
   // room for the region: the budget minus what stays live across steps
@@ -1525,7 +1677,12 @@ int lms_host_reserve(lms_ctx* c, size_t total) {
     const size_t grow = std::min(chunk, total - c->host_reserved);
     void* q = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    cudaError_t e = cudaHostAlloc(&q, grow, cudaHostAllocPortable | cudaHostAllocMapped);
+    cudaError_t e;
+    {
+      NumaPrefer np(c->numa_node);
+      e = cudaHostAlloc(&q, grow, cudaHostAllocPortable | cudaHostAllocMapped);
+    }
+    if (e == cudaSuccess && c->numa_node >= 0 && page_node(q) == c->numa_node) c->chunks_on_node++;
     c->st.host_grow_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -1554,6 +1711,7 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
   for (int k = 0; k < ndim; ++k)
     if (sizes[k] < 0 || strides[k] < 0) return fail(LMS_E_INVALID, "negative size or stride");
   std::lock_guard<std::mutex> g(c->mu);
+  NvtxRange nv("lms:swap_out");
   reap_zombies(c);
   auto* h = new lms_handle();
   h->id = c->next_id++;
@@ -1574,7 +1732,10 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
   }
   if (is_zvc(codec) && (h->packed || stored % 4 != 0 || !aligned)) codec = LMS_CODEC_RAW_SM;
   if (codec == LMS_CODEC_RAW_SM && !h->packed && !aligned) codec = LMS_CODEC_RAW_CE;
-  if (h->packed) codec = LMS_CODEC_RAW_SM;  // fused pack straight into pinned memory
+  // a strided view is packed on its way out: TMA into the D2H staging block +
+  // copy engine when staging is available (decided below), else one SIMT pack
+  // kernel straight into pinned memory
+  if (h->packed) codec = LMS_CODEC_RAW_SM;
   h->codec = codec;
   h->host_bytes = is_zvc(codec) ? zvc_bound(stored / 4) : (stored ? stored : 16);
   int rc = host_alloc_locked(c, h->host_bytes, reinterpret_cast<void**>(&h->host));
@@ -1593,10 +1754,15 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
       CK(cudaMemcpyAsync(h->host, src, stored, cudaMemcpyDeviceToHost, s));
       h->wire = stored;
     } else if (codec == LMS_CODEC_RAW_SM) {
-      if (h->packed)
-        rc = launch_layout<true>(c, h->host, static_cast<const char*>(src), ndim, sizes, strides, elem_size, s);
-      else
+      if (h->packed) {
+        rc = staged_pack_d2h(c, h->host, static_cast<const char*>(src), ndim, sizes, strides, elem_size, s);
+        if (rc == 0)
+          h->codec = LMS_CODEC_RAW_CE;   // packed in HBM, moved by the copy engine
+        else if (rc == 1)
+          rc = launch_layout<true>(c, h->host, static_cast<const char*>(src), ndim, sizes, strides, elem_size, s);
+      } else {
         rc = launch_copy(c, h->host, static_cast<const char*>(src), stored, s);
+      }
       h->wire = stored;
     } else {
       rc = launch_zvc_encode(c, static_cast<const uint32_t*>(src), stored / 4, h->host, s, true,
@@ -1642,6 +1808,7 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
   if (!c || !h) return fail(LMS_E_INVALID, "null argument");
   if (!dst && h->numel > 0) return fail(LMS_E_INVALID, "null destination");
   std::lock_guard<std::mutex> g(c->mu);
+  NvtxRange nv("lms:swap_in");
   if (h->released) return fail(LMS_E_STATE, "swap_in of a released handle");
   cudaStream_t s = c->h2d;
   // gate: the control op (everything enqueued on the trigger stream) and the swap-out
@@ -1677,7 +1844,9 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
       if (is_zvc(h->codec)) return fail(LMS_E_INVALID, "ZVC handles restore to their own layout");
       if (!h->packed)
         return fail(LMS_E_INVALID, "a dense view restores only into its own strides (pass NULL)");
-      rc = launch_layout<false>(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
+      rc = staged_unpack_h2d(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
+      if (rc == 1)
+        rc = launch_layout<false>(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
       wire = stored;
     } else if (is_zvc(h->codec)) {
       // zero-copy: the decode kernel reads the compressed stream straight out
@@ -1881,6 +2050,8 @@ int lms_stats(lms_ctx* c, lms_stats_t* out) {
   s.host_in_use = c->host_used;
   s.host_peak = c->host_peak;
   s.host_reserved = c->host_reserved;
+  s.numa_node = c->numa_node;
+  s.n_host_chunks_on_node = c->chunks_on_node;
   double d2h = 0, h2d = 0;
   for (auto& r : c->recs) {
     if (cudaEventQuery(r.end) != cudaSuccess) continue;

@@ -54,7 +54,8 @@ class _Stats(ctypes.Structure):
         ("swap_wait_ms", ctypes.c_double), ("pool_driver_ms", ctypes.c_double),
         ("alloc_wait_ms", ctypes.c_double), ("host_grow_ms", ctypes.c_double),
         ("n_host_grow", ctypes.c_uint64), ("n_scratch_grow", ctypes.c_uint64),
-        ("unmap_ms", ctypes.c_double), ("map_ms", ctypes.c_double), ("access_ms", ctypes.c_double)]
+        ("unmap_ms", ctypes.c_double), ("map_ms", ctypes.c_double), ("access_ms", ctypes.c_double),
+        ("numa_node", ctypes.c_int64), ("n_host_chunks_on_node", ctypes.c_uint64)]
 
 
 class _Xfer(ctypes.Structure):
@@ -325,6 +326,13 @@ class Context:
         if not h.released:
             h.released = True
             _check(lib().lms_handle_release(self.ptr, h.ptr), "lms_handle_release")
+
+    def handle_codec(self, h: SwapHandle) -> int:
+        """The transfer path a swap-out took (CODEC_*; strided views packed in HBM
+        and moved by the copy engine report CODEC_RAW_CE)."""
+        c = ctypes.c_int()
+        _check(lib().lms_handle_info(h.ptr, None, None, None, ctypes.byref(c)), "lms_handle_info")
+        return c.value
 
     def wire_bytes(self, h: SwapHandle) -> int:
         w = ctypes.c_uint64()

@@ -93,6 +93,7 @@ class _Saved:
     is_param: bool
     packs: list = field(default_factory=list)   # pack indices that saved it
     zero_frac: float = 0.0
+    zx_ratio: float = 1.0
 
 
 @dataclass
@@ -157,6 +158,43 @@ class _SavedInfo:
     nbytes: int
     swapped: bool
     zero_frac: float = 0.0
+    zx_ratio: float = 1.0
+
+
+def zx_ratio_estimate(t, max_words: int = 1 << 20) -> float:
+    """Wire bytes / tensor bytes the ZX codec (ZVC v3 with exponent planes,
+    kernels.cuh) would need, computed with the codec's own per-tile rules on
+    the tensor's first ``max_words`` 32-bit words (whole 4096-word tiles)."""
+    if not t.numel() or t.element_size() != 4 or not t.is_contiguous():
+        return 1.0
+    w = t.detach().reshape(-1).view(torch.int32)
+    n = min(w.numel(), max_words) // 4096 * 4096
+    if n == 0:
+        return 1.0
+    w = w[:n].view(-1, 4096).long() & 0xFFFFFFFF
+    nz = w != 0
+    e7 = (w >> 24) & 0x7F
+    s = w >> 31
+    cnt = nz.sum(1)
+
+    def pad16(x):
+        return (x + 15) // 16 * 16
+
+    def bits(r):
+        return torch.where(r > 0, torch.floor(torch.log2(r.clamp(min=1).double())) + 1, torch.zeros_like(r.double()))
+
+    raw = torch.full_like(cnt, 16384).double()
+    mask = (512 + pad16(4 * cnt)).double()
+    kd = bits(e7.max(1).values - e7.min(1).values)
+    sd = (s.max(1).values != s.min(1).values).double()
+    expd = pad16(torch.full_like(cnt, 3 * 4096)).double() + pad16(torch.ceil(4096 * (kd + sd) / 8))
+    big, small = torch.full_like(e7, 127), torch.zeros_like(e7)
+    km = bits(torch.where(nz, e7, small).max(1).values - torch.where(nz, e7, big).min(1).values)
+    sm = (torch.where(nz, s, small).max(1).values != torch.where(nz, s, torch.ones_like(s)).min(1).values).double()
+    expm = 512 + pad16(3 * cnt).double() + pad16(torch.ceil(cnt * (km + sm) / 8))
+    expm = torch.where(cnt > 0, expm, mask)
+    best = torch.minimum(torch.minimum(raw, mask), torch.minimum(expd, expm))
+    return float((best.sum() + 8 * best.numel()) / (4.0 * n))
 
 
 class _Capture:
@@ -167,6 +205,7 @@ class _Capture:
         self.keep = []         # strong refs so addresses stay unique during capture
         self.consumer = {}     # pack idx -> autograd node that unpacked it
         self.zero_frac = []    # pack idx -> share of zero words (capture-time contents)
+        self.zx_ratio = []     # pack idx -> ZX codec wire/tensor bytes (capture-time contents)
 
     def pack(self, t):
         k = len(self.packs)
@@ -182,6 +221,7 @@ class _Capture:
                 w = w[:: w.numel() >> 22]
             zf = 1.0 - float(torch.count_nonzero(w)) / w.numel()
         self.zero_frac.append(zf)
+        self.zx_ratio.append(zx_ratio_estimate(t) if not isinstance(t, torch.nn.Parameter) else 1.0)
         t = t.detach()   # no tensor -> grad_fn -> saved -> tensor cycle (see SwapExecutor.pack)
         self.keep.append(t)
         return (k, t)
@@ -299,7 +339,8 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
                 producer = grad_fn
             else:
                 producer = "self"  # non-differentiable output of the saving op
-            s = _Saved(len(saved), nbytes, producer, is_param, zero_frac=cap.zero_frac[k])
+            s = _Saved(len(saved), nbytes, producer, is_param, zero_frac=cap.zero_frac[k],
+                       zx_ratio=cap.zx_ratio[k])
             by_key[key] = s
             saved.append(s)
         s.packs.append(k)
@@ -412,7 +453,7 @@ def build_plan(g: CompGraph, meta: dict, cfg: RewriteConfig, capture_batch: int,
     swapped_tids = {tid for _, _, tid in rep.edges_rewritten}
     pack_saved = meta["pack_saved"]
     saved_info = [_SavedInfo(s.tid, s.nbytes, meta["saved_tensor_id"].get(s.tid) in swapped_tids,
-                             s.zero_frac) for s in meta["saved"]]
+                             s.zero_frac, s.zx_ratio) for s in meta["saved"]]
 
     # swap-in nodes -> groups
     groups = []
@@ -708,14 +749,17 @@ class SwapExecutor:
         # and "issue" {gid: (plan clock at the swap-in, bytes)}
         self.probe: dict | None = None
 
-    # ZVC pays off once enough words are zero: its stream is 1/32 bitmask plus
-    # the nonzero words, moved by SMs at ~51 GB/s where the copy engine does
-    # ~55.5 (profiles/README.md), so it wins above ~11 % zero words
-    ZVC_MIN_ZERO_FRAC = 0.15
+    # The codecs move encoded bytes with SM kernels at ~50 GB/s where the copy
+    # engine moves raw bytes at ~55.5 (profiles/README.md), so an encoded
+    # transfer wins once its stream is below ~0.9 of the tensor.  The capture
+    # step measured each saved tensor's ZX ratio with the codec's own tile rules
+    # (ReLU outputs ~0.45: zero masks, no sign bit; BN inputs ~0.87: 3-4
+    # exponent bits instead of 8).
+    ZX_MAX_RATIO = 0.85
 
     def _codec_for(self, si: int, t) -> str:
         if self.codec == "auto":
-            return "zvc" if self.plan.saved[si].zero_frac >= self.ZVC_MIN_ZERO_FRAC else "ce"
+            return "zx" if self.plan.saved[si].zx_ratio <= self.ZX_MAX_RATIO else "ce"
         if isinstance(self.codec, str):
             return self.codec
         return self.codec.get(si, "ce")
@@ -804,7 +848,9 @@ class SwapExecutor:
         self.forward_swaps = fwd
         hooks = []
         loss = None
+        nvtx = torch.cuda.nvtx
         try:
+            nvtx.range_push("lms:forward")
             with torch.autograd.graph.saved_tensors_hooks(pack, unpack):
                 if fwd is None:
                     loss = forward_fn()
@@ -812,6 +858,7 @@ class SwapExecutor:
                     with fwd:
                         loss = forward_fn()
                     fwd.finish()
+            nvtx.range_pop()
             if k_counter[0] != plan.n_packs:
                 raise RuntimeError(f"step saved {k_counter[0]} tensors but the plan was captured with "
                                    f"{plan.n_packs}; re-capture the plan for this model/step")
@@ -829,7 +876,9 @@ class SwapExecutor:
                         hooks.append(n.register_hook(_issuer(issue, gids)))
             for gid in plan.bwd_start_groups:
                 issue(gid)
+            nvtx.range_push("lms:backward")
             loss.backward()
+            nvtx.range_pop()
         except BaseException:
             # a failed step (e.g. the budget is too small) must not pin the
             # graph, the swapped-in tensors or the host copies: the exception's
@@ -940,7 +989,7 @@ class LMS:
         return timings
 
     def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8, 12, 16, 24, 32, 48, 64, 96), margin: float = 0.005,
-                     require_faster: bool = True) -> dict:
+                     require_faster: bool = True, steps: int = 5, agree=None) -> dict:
         """Memory-aware control-op windows, one per swap-in (an extension: the
         paper leaves choosing lb open).  Every candidate control
         op comes from the reference's own strategy run with a wider window
@@ -960,7 +1009,14 @@ class LMS:
         timed against the untouched plan; the set shrinks by a third until a replay
         fits and is faster, or dropped.  The model parameters move by the
         probe and trial steps (like ``autotune``).  Returns a summary dict;
-        ``{}`` changes nothing (no room, or no static plan to measure)."""
+        ``{}`` changes nothing (no room, or no static plan to measure).
+
+        Each replay times ``steps`` steps (median and spread reported).  The
+        winning trial's recorded placement is kept: the next steps replay the
+        very placement that was timed.  Under DDP every rank must take the same
+        number of steps: ``agree(value, op)`` (an all-reduce, op "max"/"min")
+        makes every timing- and memory-dependent decision common to all ranks
+        (slowest rank's times, any rank's failure)."""
         from dataclasses import replace
         import numpy as np
         if not self.static_plan or self.plan is None:
@@ -978,6 +1034,9 @@ class LMS:
         if not ranks:
             return {}
         # step 0 of the plan runs dynamic; step 1 records with the probe on
+        def common(v, op):
+            return v if agree is None else agree(v, op)
+
         self._drop_step_plan()
         while self._plan_step != 1:
             self.step(x, y)
@@ -987,7 +1046,8 @@ class LMS:
         finally:
             self._exec.probe = None
         torch.cuda.synchronize()
-        if self.plan_note != "region":
+        if common(1.0 if self.plan_note == "region" else 0.0, "min") < 0.5:
+            self._drop_step_plan()
             return {}
         info = self.ctx.plan_info()
         items = self.ctx.plan_items()
@@ -1032,28 +1092,37 @@ class LMS:
                 else:
                     hi = mid
             keep = lo
-        # the model predicts; a replayed step decides: re-record with the moves,
+        # each rank models its own recorded step; the trial schedule is common
+        keep = int(common(float(keep), "min"))
+        # the model predicts; replayed steps decide: re-record with the moves,
         # keep them if the placement fits at the physical-release lifetimes
         # (alpha 1: no block reused before its swap-out copy landed) and the
-        # replayed step is faster than the untouched plan's; else halve the set
+        # replayed steps are faster than the untouched plan's; else shrink the set
         orig = self.plan
-        base_ms = self._timed_replay(x, y)
-        trials = {}
+        base = self._timed_replay(x, y, steps, agree)
+        base_ms = base["ms"] if base else None
+        trials, spreads = {}, {"base": base["spread"] if base else None}
         chosen = 0
         while keep > 0 and base_ms is not None:
             self._set_plan(retarget(orig, {m[0]: m[4] for m in moved[:keep]}))
-            ms = self._timed_replay(x, y)
-            trials[keep] = ms
-            if ms is not None and (ms < base_ms or not require_faster):
+            r = self._timed_replay(x, y, steps, agree)
+            trials[keep] = r["ms"] if r else None
+            spreads[keep] = r["spread"] if r else None
+            if r is not None and (r["ms"] < base_ms or not require_faster):
                 chosen = keep
                 break
             keep = keep * 2 // 3
         if not chosen:
+            # the untouched plan won: replay it again so its recorded placement is the one kept
             self._set_plan(orig)
-        self._drop_step_plan()
+            again = self._timed_replay(x, y, steps, agree) if base_ms is not None else None
+            final = again["ms"] if again else None
+        else:
+            final = trials[chosen]   # the winner's recording is the live plan: kept as is
         return {"moved": chosen, "of": len(issue), "modelled": len(moved),
                 "moved_bytes": sum(m[3] for m in moved[:chosen]),
-                "base_ms": base_ms, "trials": trials, "peak_before": start_peak,
+                "base_ms": base_ms, "trials": trials, "spread_ms": spreads, "final_ms": final,
+                "steps_per_trial": steps, "peak_before": start_peak,
                 "limit": limit, "lower_bound": info["lower_bound_bytes"]}
 
     def _set_plan(self, plan: SwapPlan):
@@ -1061,28 +1130,40 @@ class LMS:
         self._exec = SwapExecutor(self.ctx, plan, self.codec)
         self._drop_step_plan()
 
-    def _timed_replay(self, x, y, steps: int = 2):
-        """Re-record the current plan and time ``steps`` replayed steps (ms per step); None if the
-        placement does not fit at physical-release lifetimes or a step hits the budget."""
+    def _timed_replay(self, x, y, steps: int = 5, agree=None):
+        """Re-record the current plan (3 steps: dynamic, recorded, first replay) and
+        time ``steps`` replayed ones.  Returns {"ms": median ms per step, "spread":
+        (min, max)} or None if the placement does not fit at physical-release
+        lifetimes or a step hits the budget.  The step count is fixed, so DDP ranks
+        stay in step; ``agree`` makes the outcome common (slowest rank, any failure)."""
         self._drop_step_plan()
+        per = None
         try:
-            while self._plan_step < 3:
+            for _ in range(3):
                 self.step(x, y)
-            if self.plan_note != "region" or self.ctx.plan_info()["alpha"] < 1.0:
-                return None
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            fits = self.plan_note == "region" and self.ctx.plan_info()["alpha"] >= 1.0
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
             torch.cuda.synchronize()
-            e0.record()
-            for _ in range(steps):
+            evs[0].record()
+            for k in range(steps):
                 self.step(x, y)
-            e1.record()
+                evs[k + 1].record()
             torch.cuda.synchronize()
-            return e0.elapsed_time(e1) / steps
+            per = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(steps)) if fits else None
         except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
+            if agree is not None:
+                raise     # a rank that failed mid-step cannot rejoin its peers' collectives
             self.optimizer.zero_grad(set_to_none=True)
             torch.cuda.synchronize()
             self.ctx.synchronize()
+            self._drop_step_plan()
+        if agree is not None:
+            if agree(0.0 if per is None else 1.0, "min") < 0.5:
+                return None
+            per = [agree(v, "max") for v in per]
+        if per is None:
             return None
+        return {"ms": per[len(per) // 2], "spread": (per[0], per[-1])}
 
     def trace_events(self):
         """The last steps' measured transfers as the reference's ``TraceEvent``s

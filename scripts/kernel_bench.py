@@ -161,17 +161,32 @@ def main():
         res["swap_sm_dense"] = swap_rates("sm", dense)
         res["swap_zvc_relu"] = swap_rates("zvc", relu)
         res["swap_zvc_dense"] = swap_rates("zvc", dense)
+        res["swap_zx_relu"] = swap_rates("zx", relu)
+        res["swap_zx_dense"] = swap_rates("zx", dense)
         res["swap_ce_relu"] = swap_rates("ce", relu)
+        # strided views (not dense in memory): channels-last view of NCHW and a channel slice
+        xv = torch.randn(max(1, n // (64 * 56 * 56)), 64, 56, 56, device=dev)
+        res["swap_ce_channels_last_view"] = swap_rates("ce", xv.permute(0, 2, 3, 1))
+        res["swap_ce_channel_slice"] = swap_rates("ce", xv[:, 8:40])
 
     if on("zvc"):
+        # HBM-side codec rates: one pass reads the tensor and writes the encoded
+        # stream (decode: the reverse); algorithmic HBM bytes = tensor + wire bytes
         relu = torch.relu(torch.randn(n, device=dev))
-        enc = torch.empty(ctx.zvc_bound(n), dtype=torch.uint8, device=dev)
-        t = timed(lambda: ctx.zvc_encode(relu, enc))
-        res["zvc_encode_hbm"] = {"logical_gbs": nbytes / t / 1e9, "ms": t * 1e3}
-        outd = torch.empty_like(relu)
-        t = timed(lambda: ctx.zvc_decode(enc, outd))
-        assert torch.equal(outd, relu)
-        res["zvc_decode_hbm"] = {"logical_gbs": nbytes / t / 1e9, "ms": t * 1e3}
+        dense = torch.randn(n, device=dev)
+        for name, src, exps in (("zvc", relu, False), ("zx", relu, True), ("zx_dense", dense, True)):
+            enc = torch.empty(ctx.zvc_bound(n), dtype=torch.uint8, device=dev)
+            t = timed(lambda: ctx.zvc_encode(src, enc, exponents=exps))
+            torch.cuda.synchronize()
+            wire = ctx.zvc_encoded_size(enc.cpu())
+            res[f"{name}_encode_hbm"] = {"logical_gbs": nbytes / t / 1e9, "hbm_gbs": (nbytes + wire) / t / 1e9,
+                                         "frac_hbm": (nbytes + wire) / t / 1e9 / hbm_peak,
+                                         "wire_frac": wire / nbytes, "ms": t * 1e3}
+            outd = torch.empty_like(src)
+            t = timed(lambda: ctx.zvc_decode(enc, outd))
+            assert torch.equal(outd.view(torch.int32), src.view(torch.int32))
+            res[f"{name}_decode_hbm"] = {"logical_gbs": nbytes / t / 1e9, "hbm_gbs": (nbytes + wire) / t / 1e9,
+                                         "frac_hbm": (nbytes + wire) / t / 1e9 / hbm_peak, "ms": t * 1e3}
 
     print(json.dumps(res, indent=1))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

@@ -128,3 +128,29 @@ def test_zvc_zero_copy_paths(lms_ctx, bulk, ctas):
             lms_ctx.release(h)
     finally:
         lms_ctx.set_tuning(sms, 1)
+
+
+def test_strided_swap_goes_through_staging(lms_ctx):
+    """A non-dense view (channel slice, > one 32 MiB staging slab) is packed in HBM
+    by the TMA kernels into the D2H channel's staging block and moved by the copy
+    engine; restoring into another strided view unpacks through the H2D block."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    base = torch.randn(48, 96, 56, 56, device="cuda", generator=g)
+    v = base[:, 16:80]                       # 48 x 64 x 56 x 56 fp32 = 37.6 MiB, not dense
+    want = v.contiguous()
+    lms_ctx.trace_clear()
+    h = lms_ctx.swap_out(v, "ce")
+    assert lms_ctx.handle_codec(h) == rt.CODEC_RAW_CE
+    out = lms_ctx.swap_in(h)                  # natural (contiguous) restore: copy engine
+    lms_ctx.wait(h)
+    big = torch.zeros(48, 128, 56, 56, device="cuda")
+    dst = big[:, 32:96]                       # strided destination: staged H2D + TMA unpack
+    lms_ctx.swap_in(h, dst=dst)
+    lms_ctx.wait(h)
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+    assert torch.equal(dst, want)
+    assert float(big[:, :32].abs().sum()) == 0.0 and float(big[:, 96:].abs().sum()) == 0.0
+    lms_ctx.release(h)
+    st = lms_ctx.stats()
+    assert st["kernel_launches"] >= 4        # >= 2 pack slabs + 2 unpack slabs
