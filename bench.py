@@ -803,6 +803,10 @@ def main():
                  "timed_pool_driver_ms": round(st1["pool_driver_ms"] - st0["pool_driver_ms"], 1),
                  "plan_info": ctx.plan_info()},
         "host_link": {k: round(v, 2) for k, v in link.items()},
+        "link_floor": link_floor(link, d2h_b / steps, h2d_b / steps, swap_ms / steps,
+                                 noswap_ms / steps * bs / b0 if noswap_ms and b0 else None),
+        "numa": {"gpu_node": st1.get("numa_node"), "pinned_chunks_on_node": st1.get("n_host_chunks_on_node"),
+                 "pinned_chunks": st1.get("n_host_grow")},
         "transfer_paths": paths,
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -823,6 +827,29 @@ def main():
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+
+
+def link_floor(link, d2h_bytes, h2d_bytes, step_ms, compute_ms):
+    """How close the step is to what the host link allows for its bytes.
+
+    simplex: both directions one after the other at their own peaks; duplex:
+    both at once (bounded by each direction's peak and the measured duplex
+    total); the step cannot beat the larger of the duplex floor and the compute
+    it must run (the no-swap step's time scaled to this batch)."""
+    if not link or not link.get("d2h") or not link.get("h2d"):
+        return None
+    t_o = d2h_bytes / (link["d2h"] * 1e9) * 1e3
+    t_i = h2d_bytes / (link["h2d"] * 1e9) * 1e3
+    duplex = max(t_o, t_i, (d2h_bytes + h2d_bytes) / (link.get("duplex_total", 1e-9) * 1e9) * 1e3)
+    out = {"d2h_ms": round(t_o, 1), "h2d_ms": round(t_i, 1), "simplex_floor_ms": round(t_o + t_i, 1),
+           "duplex_floor_ms": round(duplex, 1), "step_ms": round(step_ms, 1),
+           "step_over_simplex_floor": round(step_ms / (t_o + t_i), 3),
+           "step_avg_link_frac": round((d2h_bytes + h2d_bytes) / (step_ms * 1e-3) /
+                                       (link.get("duplex_total", 1e-9) * 1e9), 3)}
+    if compute_ms:
+        out["compute_ms_est"] = round(compute_ms, 1)
+        out["floor_ms"] = round(max(duplex, compute_ms), 1)
+    return out
 
 
 def unit_name(args) -> str:

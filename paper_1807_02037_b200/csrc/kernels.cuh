@@ -402,8 +402,10 @@ __device__ __forceinline__ uint32_t zvc_get_exp(const unsigned char* lo, const u
 // form, the chunk is assembled in shared memory and leaves with one bulk
 // store (TMA when use_bulk, else 16 B STG) into its fixed slot.  Double-
 // buffered: tile k+1 is built while tile k's chunk is in flight.
+template <bool kExp>
 __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __restrict__ src, uint64_t nwords,
-                                                         char* __restrict__ out, int use_bulk, int allow_exp) {
+                                                            char* __restrict__ out, int use_bulk) {
+  constexpr int allow_exp = kExp;
   extern __shared__ __align__(128) unsigned char zsm[];
   __shared__ uint32_t seg[kZvcMaskWords + 1];
   __shared__ uint32_t red[8][9];
@@ -485,30 +487,35 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
     uint32_t nnz = 0, mn_a = 127, mx_a = 0, or_a = 0, and_a = 1, mn_z = 127, mx_z = 0, or_z = 0, and_z = 1;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint32_t v = w16[r], e7 = (v >> 24) & 0x7Fu, s = v >> 31;
-      if (uint32_t(r * 256 + threadIdx.x) < nvalid) {
-        mn_a = min(mn_a, e7);
-        mx_a = max(mx_a, e7);
-        or_a |= s;
-        and_a &= s;
-      }
-      if (v) {
-        ++nnz;
-        mn_z = min(mn_z, e7);
-        mx_z = max(mx_z, e7);
-        or_z |= s;
-        and_z &= s;
+      const uint32_t v = w16[r];
+      nnz += v != 0;
+      if (kExp) {   // the top-byte ranges only matter when exponent planes are allowed
+        const uint32_t e7 = (v >> 24) & 0x7Fu, s = v >> 31;
+        if (uint32_t(r * 256 + threadIdx.x) < nvalid) {
+          mn_a = min(mn_a, e7);
+          mx_a = max(mx_a, e7);
+          or_a |= s;
+          and_a &= s;
+        }
+        if (v) {
+          mn_z = min(mn_z, e7);
+          mx_z = max(mx_z, e7);
+          or_z |= s;
+          and_z &= s;
+        }
       }
     }
     nnz = __reduce_add_sync(0xffffffffu, nnz);
-    mn_a = __reduce_min_sync(0xffffffffu, mn_a);
-    mx_a = __reduce_max_sync(0xffffffffu, mx_a);
-    or_a = __reduce_or_sync(0xffffffffu, or_a);
-    and_a = __reduce_and_sync(0xffffffffu, and_a);
-    mn_z = __reduce_min_sync(0xffffffffu, mn_z);
-    mx_z = __reduce_max_sync(0xffffffffu, mx_z);
-    or_z = __reduce_or_sync(0xffffffffu, or_z);
-    and_z = __reduce_and_sync(0xffffffffu, and_z);
+    if (kExp) {
+      mn_a = __reduce_min_sync(0xffffffffu, mn_a);
+      mx_a = __reduce_max_sync(0xffffffffu, mx_a);
+      or_a = __reduce_or_sync(0xffffffffu, or_a);
+      and_a = __reduce_and_sync(0xffffffffu, and_a);
+      mn_z = __reduce_min_sync(0xffffffffu, mn_z);
+      mx_z = __reduce_max_sync(0xffffffffu, mx_z);
+      or_z = __reduce_or_sync(0xffffffffu, or_z);
+      and_z = __reduce_and_sync(0xffffffffu, and_z);
+    }
     if (lane == 0) {
       red[warp][0] = nnz; red[warp][1] = mn_a; red[warp][2] = mx_a; red[warp][3] = or_a; red[warp][4] = and_a;
       red[warp][5] = mn_z; red[warp][6] = mx_z; red[warp][7] = or_z; red[warp][8] = and_z;

@@ -273,6 +273,7 @@ struct lms_ctx {
   // staging block owned by each copy channel, moved by the copy engine
   // (LMS_STAGE_STRIDED=0: SIMT kernels straight to/from pinned memory)
   int stage_strided = 1;
+  int enc_per_sm = 1;       // resident encode CTAs per SM (occupancy API)
   char* stage[2] = {nullptr, nullptr};   // [0] D2H channel, [1] H2D channel
   // consumer reached its wait (event on the consumer stream) vs swap-in record
   std::vector<std::pair<cudaEvent_t, int64_t>> waits;
@@ -1220,9 +1221,14 @@ int launch_zvc_encode(lms_ctx* c, const uint32_t* src, uint64_t nwords, char* ou
   const uint64_t ntiles = zvc_tiles(nwords);
   // one pass: HBM-side encodes take the whole GPU; encodes into pinned memory
   // take enough CTAs to keep the link busy without crowding the compute stream
-  int grid = sm_grid(c, int64_t(ntiles), 1);
+  // HBM side: exactly the CTAs that are resident at once (a grid-stride loop
+  // with a partial second wave would leave most SMs idle at the end)
+  int grid = int(std::min<int64_t>(int64_t(ntiles), int64_t(c->num_sms) * c->enc_per_sm));
   if (to_host) grid = int(std::min<int64_t>(int64_t(ntiles), c->zc_ctas));
-  zvc_encode_kernel<<<std::max(grid, 1), 256, kZvcEncSmemBytes, s>>>(src, nwords, out, c->use_bulk, allow_exp);
+  if (allow_exp)
+    zvc_encode_kernel<true><<<std::max(grid, 1), 256, kZvcEncSmemBytes, s>>>(src, nwords, out, c->use_bulk);
+  else
+    zvc_encode_kernel<false><<<std::max(grid, 1), 256, kZvcEncSmemBytes, s>>>(src, nwords, out, c->use_bulk);
   c->st.kernel_launches++;
   CK(cudaGetLastError());
   return LMS_OK;
@@ -1334,7 +1340,10 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
                        int(tma_transpose_smem<4>()));
   cudaFuncSetAttribute(tma_transpose_kernel<8, tt_warps<8>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(tma_transpose_smem<8>()));
-  cudaFuncSetAttribute(zvc_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcEncSmemBytes);
+  cudaFuncSetAttribute(zvc_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcEncSmemBytes);
+  cudaFuncSetAttribute(zvc_encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcEncSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->enc_per_sm, zvc_encode_kernel<true>, 256, kZvcEncSmemBytes);
+  c->enc_per_sm = std::max(1, c->enc_per_sm);
   cudaFuncSetAttribute(zvc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZvcSmemBytes);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);

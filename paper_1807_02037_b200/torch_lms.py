@@ -749,13 +749,14 @@ class SwapExecutor:
         # and "issue" {gid: (plan clock at the swap-in, bytes)}
         self.probe: dict | None = None
 
-    # The codecs move encoded bytes with SM kernels at ~50 GB/s where the copy
-    # engine moves raw bytes at ~55.5 (profiles/README.md), so an encoded
-    # transfer wins once its stream is below ~0.9 of the tensor.  The capture
-    # step measured each saved tensor's ZX ratio with the codec's own tile rules
-    # (ReLU outputs ~0.45: zero masks, no sign bit; BN inputs ~0.87: 3-4
-    # exponent bits instead of 8).
-    ZX_MAX_RATIO = 0.85
+    # The codecs move encoded bytes with SM kernels at ~51 GB/s where the copy
+    # engine moves raw bytes at ~57 (profiles/r02), so an encoded transfer wins
+    # once its stream is below ~0.9 of the tensor.  The capture step measured
+    # each saved tensor's ZX ratio with the codec's own tile rules (ReLU outputs
+    # ~0.46: zero masks, no sign bit; conv/BN outputs ~0.89: 4 exponent bits and
+    # a sign bit instead of 8 bits).  ResNet-50 at 908: ZX on both kinds
+    # 331 img/s, ZX on ReLU outputs only 321 (profiles/r02/README.md).
+    ZX_MAX_RATIO = 0.92
 
     def _codec_for(self, si: int, t) -> str:
         if self.codec == "auto":
@@ -1131,7 +1132,7 @@ class LMS:
         self._drop_step_plan()
 
     def _timed_replay(self, x, y, steps: int = 5, agree=None):
-        """Re-record the current plan (3 steps: dynamic, recorded, first replay) and
+        """Re-record the current plan (dynamic, recorded and first replayed step) and
         time ``steps`` replayed ones.  Returns {"ms": median ms per step, "spread":
         (min, max)} or None if the placement does not fit at physical-release
         lifetimes or a step hits the budget.  The step count is fixed, so DDP ranks
@@ -1139,7 +1140,15 @@ class LMS:
         self._drop_step_plan()
         per = None
         try:
-            for _ in range(3):
+            # dynamic step, recorded step, first replay; a recording whose placement
+            # did not fit is retried (at most 6 setup steps; under DDP the ranks
+            # agree on when every one of them is done)
+            for _ in range(6):
+                done = self._plan_step >= 3 or self.plan_note == "no-fit"
+                if agree is not None:
+                    done = agree(1.0 if done else 0.0, "min") > 0.5
+                if done:
+                    break
                 self.step(x, y)
             fits = self.plan_note == "region" and self.ctx.plan_info()["alpha"] >= 1.0
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]

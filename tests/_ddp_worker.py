@@ -44,9 +44,9 @@ def main():
     opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
     loss_fn = torch.nn.functional.cross_entropy
 
-    def batch(i, n=32):
+    def batch(i, n=64):
         g = torch.Generator(device="cuda").manual_seed(100 * i + rank)   # each rank its own shard
-        return (torch.randn(n, 3, 112, 112, device="cuda", generator=g),
+        return (torch.randn(n, 3, 160, 160, device="cuda", generator=g),
                 torch.randint(0, 1000, (n,), device="cuda", generator=g))
 
     def agree(v, op):
