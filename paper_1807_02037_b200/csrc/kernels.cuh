@@ -304,8 +304,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 //         nonzero words                          (ReLU outputs: ~50 % zeros)
 //   EXPD  every word split into its low 24 bits (3-byte plane) and its top
 //         byte (sign + 7 high exponent bits), the top bytes coded as
-//         (e7 - emin) in k bits plus a sign bit unless the tile's signs agree
-//   EXPM  MASK's bitmask, then EXPD's two planes over the nonzero words only
+//         (e7 - emin) in k bits plus a sign bit unless the tile's signs agree;
+//         per group of 32 consecutive words: 96 bytes of low bits, then the
+//         codes as b = k + sign bit planes (one 32-bit word per bit)
+//   EXPM  MASK's bitmask, then the nonzero words' low bytes (3 each) and their
+//         codes packed b bits each
 // (fp32 activations keep their exponents in a narrow band per tile: k is
 // typically 3-4 of 7 bits, and ReLU outputs need no sign bit.)
 //
@@ -535,9 +538,10 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
       if (bm < bytes) mode = kZMask, bytes = bm, n = z;
       if (allow_exp) {
         const uint32_t kd = zvc_nbits(red[0][2] - red[0][1]), sd = red[0][3] != red[0][4];
-        const uint32_t bd = zvc_pad16(3ull * nvalid) + zvc_pad16((uint64_t(nvalid) * (kd + sd) + 7) / 8);
+        const uint32_t ng = (nvalid + 31) / 32;
+        const uint32_t bd = 96 * ng + zvc_pad16(4ull * ng * (kd + sd));
         if (bd < bytes) mode = kZExpD, bytes = bd, n = nvalid, k = kd, sp = sd, sc = red[0][3], em = red[0][1],
-                        hoff = zvc_pad16(3ull * nvalid);
+                        hoff = 96 * ng;
         if (z) {
           const uint32_t km = zvc_nbits(red[0][6] - red[0][5]), sm = red[0][7] != red[0][8];
           const uint32_t be = 512 + zvc_pad16(3ull * z) + zvc_pad16((uint64_t(z) * (km + sm) + 7) / 8);
@@ -552,10 +556,12 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
     __syncthreads();
     const uint32_t info = pick[0], bytes = pick[1], hoff = pick[2];
     const uint32_t mode = info & 3u, k = (info >> 2) & 15u, sp = (info >> 6) & 1u, em = (info >> 8) & 0x7Fu;
-    if (mode >= kZExpD) {   // the code plane is OR-ed together: clear it (and the padding) first
+    if (mode == kZExpM) {   // the code plane is OR-ed together: clear it (and the padding) first
       for (uint32_t q = hoff / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
-      const uint32_t lo0 = mode == kZExpM ? 512u : 0u, nlo = 3u * (info >> 16);
-      for (uint32_t b = lo0 + nlo + threadIdx.x; b < hoff; b += 256) chunk[b] = 0;
+      for (uint32_t b = 512u + 3u * (info >> 16) + threadIdx.x; b < hoff; b += 256) chunk[b] = 0;
+    } else if (mode == kZExpD) {   // whole words per 32-word group: only the plane's tail padding
+      const uint32_t used = hoff + 4 * ((nvalid + 31) / 32) * (k + sp);
+      for (uint32_t q = used / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
     }
     if (mode == kZMask || mode == kZExpM) {
 #pragma unroll
@@ -585,11 +591,27 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
       const uint32_t z = seg[kZvcMaskWords];
       if (threadIdx.x < ((z + 3) & ~3u) - z) cw[kZvcMaskWords + z + threadIdx.x] = 0u;
     } else if (mode == kZExpD) {
+      // warp-cooperative: a warp's 32 consecutive words are one group -- their low
+      // 24 bits are 96 contiguous bytes (24 aligned words, gathered by shuffles)
+      // and their codes are b ballots (bit planes), no shared-memory atomics
       uint32_t* hi = reinterpret_cast<uint32_t*>(chunk + hoff);
+      const uint32_t b = k + sp;
+      const uint32_t a = (4 * lane) / 3, off = 4 * lane - 3 * a;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        const uint32_t j = r * 256 + threadIdx.x;
-        if (j < nvalid) zvc_put_exp(chunk, hi, j, w16[r], k, sp, em);
+        const uint32_t g = r * 8 + warp;
+        if (32 * g >= nvalid) break;   // warp-uniform
+        const bool valid = g * 32 + lane < nvalid;
+        const uint32_t v = w16[r];
+        const uint32_t lo = v & 0xFFFFFFu;
+        const uint32_t la = __shfl_sync(0xffffffffu, lo, a & 31), lb = __shfl_sync(0xffffffffu, lo, (a + 1) & 31);
+        const uint64_t cat = uint64_t(la) | (uint64_t(lb) << 24);
+        if (lane < 24) cw[g * 24 + lane] = uint32_t(cat >> (8 * off));
+        const uint32_t code = valid ? ((((v >> 24) & 0x7Fu) - em) | (sp ? (v >> 31) << k : 0u)) : 0u;
+        for (uint32_t q = 0; q < b; ++q) {
+          const uint32_t plane = __ballot_sync(0xffffffffu, (code >> q) & 1u);
+          if (lane == 0) hi[g * b + q] = plane;
+        }
       }
     } else {
       uint32_t* hi = reinterpret_cast<uint32_t*>(chunk + hoff);
@@ -691,7 +713,7 @@ __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict_
       if (warp == 0) zvc_seg_scan(seg, lane);
       __syncthreads();
     }
-    const uint32_t hoff = mode == kZExpD ? zvc_pad16(3ull * n) : 512 + zvc_pad16(3ull * n);
+    const uint32_t hoff = mode == kZExpD ? 96 * ((n + 31) / 32) : 512 + zvc_pad16(3ull * n);
     const unsigned char* lo = chunk + (mode == kZExpM ? 512 : 0);
     const uint32_t* hi = reinterpret_cast<const uint32_t*>(chunk + hoff);
     const uint64_t base = t * kZvcTileWords;
@@ -703,7 +725,15 @@ __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict_
       if (mode == kZRaw) {
         v = cw[j < kZvcTileWords ? j : 0];
       } else if (mode == kZExpD) {
-        v = i < nwords ? zvc_get_exp(lo, hi, j, k, sp, sc, em) : 0u;
+        // group g = r*8 + warp: its low bytes at 96 g, its code planes at words b g .. b g + b-1
+        const uint32_t g = r * 8 + warp, b = k + sp, sh = (3 * lane & 3) * 8;
+        const uint32_t* lw = cw + g * 24 + (3 * lane) / 4;
+        const uint32_t low = ((lw[0] >> sh) | (sh > 8 ? lw[1] << (32 - sh) : 0u)) & 0xFFFFFFu;
+        uint32_t code = 0;
+        for (uint32_t q = 0; q < b; ++q) code |= ((hi[g * b + q] >> lane) & 1u) << q;
+        const uint32_t e7 = em + (code & ((1u << k) - 1u));
+        const uint32_t sg = sp ? (code >> k) & 1u : sc;
+        v = i < nwords ? (((sg << 7 | e7) << 24) | low) : 0u;
       } else {
         const uint32_t m = cw[r * 8 + warp];
         const uint32_t p = seg[r * 8 + warp] + __popc(m & lt);

@@ -1023,10 +1023,13 @@ int launch_tma_transpose(lms_ctx* c, char* dst, const char* src, int nd, const i
   return 0;
 }
 
-// pack (dst contiguous) or unpack (dst strided); either side may be mapped host memory
+// pack (dst contiguous) or unpack (dst strided); either side may be mapped host
+// memory.  `mem`: 0 both sides in HBM, 1 one side is host memory, -1 unknown
+// (the public entry points: one cudaPointerGetAttributes per side)
+enum { kMemDevice = 0, kMemHost = 1, kMemUnknown = -1 };
 template <bool PACK>
 int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_t* sizes_in,
-                  const int64_t* strides_in, int elem, cudaStream_t s) {
+                  const int64_t* strides_in, int elem, cudaStream_t s, int mem) {
   int64_t sizes[LMS_MAX_DIMS + 1], strides[LMS_MAX_DIMS + 1];
   // squeeze size-1 dims; widen 16-byte elements into two 8-byte words
   int nd = 0;
@@ -1063,7 +1066,8 @@ int launch_layout(lms_ctx* c, char* dst, const char* src, int ndim, const int64_
     default: KERNEL<PACK, 8><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                 \
   }
   const int last = nd - 1;
-  if (!is_host_ptr(dst) && !is_host_ptr(src)) {
+  if (mem == kMemUnknown) mem = (is_host_ptr(dst) || is_host_ptr(src)) ? kMemHost : kMemDevice;
+  if (mem == kMemDevice) {
     int rc = strides[last] == 1 ? launch_tma_rows<PACK>(c, dst, src, nd, sizes, strides, elem, s)
                                 : launch_tma_transpose<PACK>(c, dst, src, nd, sizes, strides, elem, s);
     if (rc <= 0) return rc;
@@ -1163,7 +1167,7 @@ int staged_pack_d2h(lms_ctx* c, char* host, const char* src, int ndim, const int
   std::memcpy(sz, sizes, sizeof(int64_t) * ndim);
   for (int64_t a = 0; a < sizes[k0]; a += per) {
     sz[k0] = std::min(per, sizes[k0] - a);
-    int rc = launch_layout<true>(c, stg, src + a * strides[k0] * elem, ndim, sz, strides, elem, s);
+    int rc = launch_layout<true>(c, stg, src + a * strides[k0] * elem, ndim, sz, strides, elem, s, kMemDevice);
     if (rc) return rc;
     CK(cudaMemcpyAsync(host + a * row, stg, uint64_t(sz[k0]) * row, cudaMemcpyDeviceToHost, s));
   }
@@ -1185,7 +1189,8 @@ int staged_unpack_h2d(lms_ctx* c, char* dst, const char* host, int ndim, const i
   for (int64_t a = 0; a < sizes[k0]; a += per) {
     sz[k0] = std::min(per, sizes[k0] - a);
     CK(cudaMemcpyAsync(stg, host + a * row, uint64_t(sz[k0]) * row, cudaMemcpyHostToDevice, s));
-    int rc = launch_layout<false>(c, dst + a * dst_strides[k0] * elem, stg, ndim, sz, dst_strides, elem, s);
+    int rc = launch_layout<false>(c, dst + a * dst_strides[k0] * elem, stg, ndim, sz, dst_strides, elem, s,
+                                  kMemDevice);
     if (rc) return rc;
   }
   return 0;
@@ -1768,7 +1773,8 @@ int lms_swap_out(lms_ctx* c, const void* src, const int64_t* sizes, const int64_
         if (rc == 0)
           h->codec = LMS_CODEC_RAW_CE;   // packed in HBM, moved by the copy engine
         else if (rc == 1)
-          rc = launch_layout<true>(c, h->host, static_cast<const char*>(src), ndim, sizes, strides, elem_size, s);
+          rc = launch_layout<true>(c, h->host, static_cast<const char*>(src), ndim, sizes, strides, elem_size, s,
+                                   kMemHost);
       } else {
         rc = launch_copy(c, h->host, static_cast<const char*>(src), stored, s);
       }
@@ -1855,7 +1861,8 @@ int lms_swap_in(lms_ctx* c, lms_handle* h, void* dst, const int64_t* dst_strides
         return fail(LMS_E_INVALID, "a dense view restores only into its own strides (pass NULL)");
       rc = staged_unpack_h2d(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
       if (rc == 1)
-        rc = launch_layout<false>(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s);
+        rc = launch_layout<false>(c, static_cast<char*>(dst), h->host, h->ndim, h->sizes, dst_strides, h->elem, s,
+                                  kMemHost);
       wire = stored;
     } else if (is_zvc(h->codec)) {
       // zero-copy: the decode kernel reads the compressed stream straight out
@@ -1960,7 +1967,7 @@ int lms_pack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, const
   if (!c || !dst || !src) return fail(LMS_E_INVALID, "null argument");
   if (ndim < 0 || ndim > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "ndim out of range");
   return launch_layout<true>(c, static_cast<char*>(dst), static_cast<const char*>(src), ndim, sizes, strides,
-                             elem_size, static_cast<cudaStream_t>(stream));
+                             elem_size, static_cast<cudaStream_t>(stream), kMemUnknown);
 }
 
 int lms_unpack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, const int64_t* strides, int ndim,
@@ -1969,7 +1976,7 @@ int lms_unpack(lms_ctx* c, void* dst, const void* src, const int64_t* sizes, con
   if (!c || !dst || !src) return fail(LMS_E_INVALID, "null argument");
   if (ndim < 0 || ndim > LMS_MAX_DIMS) return fail(LMS_E_INVALID, "ndim out of range");
   return launch_layout<false>(c, static_cast<char*>(dst), static_cast<const char*>(src), ndim, sizes, strides,
-                              elem_size, static_cast<cudaStream_t>(stream));
+                              elem_size, static_cast<cudaStream_t>(stream), kMemUnknown);
 }
 
 size_t lms_zvc_bound(size_t nwords) { return zvc_bound(nwords); }

@@ -187,7 +187,7 @@ def zx_ratio_estimate(t, max_words: int = 1 << 20) -> float:
     mask = (512 + pad16(4 * cnt)).double()
     kd = bits(e7.max(1).values - e7.min(1).values)
     sd = (s.max(1).values != s.min(1).values).double()
-    expd = pad16(torch.full_like(cnt, 3 * 4096)).double() + pad16(torch.ceil(4096 * (kd + sd) / 8))
+    expd = 96 * 128 + pad16(4 * 128 * (kd + sd))
     big, small = torch.full_like(e7, 127), torch.zeros_like(e7)
     km = bits(torch.where(nz, e7, small).max(1).values - torch.where(nz, e7, big).min(1).values)
     sm = (torch.where(nz, s, small).max(1).values != torch.where(nz, s, torch.ones_like(s)).min(1).values).double()
