@@ -745,7 +745,8 @@ def main():
         roof = {"bound": "host-link", "kernel": dom_key + (" (zvc_encode_kernel/zvc_decode_kernel)"
                                                           if ("zvc" in dom_key or "zx" in dom_key) else ""),
                 "achieved": achieved, "peak": round(dom_peak, 2) if dom_peak else None, "unit": "GB/s",
-                "frac": round(achieved / dom_peak, 4) if dom_peak else None, "traffic": None,
+                "frac": round(achieved / dom_peak, 4) if dom_peak else None,
+                "traffic": ncu_traffic("zvc_decode_kernel" if dom_key.startswith("h2d") else "zvc_encode_kernel"),
                 "peak_source": "pinned copy-engine copy of 512 MiB measured in this run (host link has no "
                                "MEASURED_PEAKS entry)",
                 "algorithmic_bytes": "wire bytes of each transfer (compressed size for ZVC)"}
@@ -827,6 +828,21 @@ def main():
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of the dominant swap kernel from the committed ncu
+    capture (profiles/r02/zvc_swap_traffic.json: a 256 MiB tensor swapped
+    zero-copy), next to the launch's algorithmic HBM bytes (the tensor)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02", "zvc_swap_traffic.json")))
+        k = d[kernel]
+        return {"dram_bytes_per_launch": round(k["dram_bytes_per_launch"]),
+                "algorithmic_hbm_bytes_per_launch": d["tensor_bytes"],
+                "ratio": round(k["dram_bytes_per_launch"] / d["tensor_bytes"], 3),
+                "source": "profiles/r02/zvc_swap_traffic.json (ncu dram__bytes_read.sum + dram__bytes_write.sum)"}
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def link_floor(link, d2h_bytes, h2d_bytes, step_ms, compute_ms):

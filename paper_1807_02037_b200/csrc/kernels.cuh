@@ -304,9 +304,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 //         nonzero words                          (ReLU outputs: ~50 % zeros)
 //   EXPD  every word split into its low 24 bits (3-byte plane) and its top
 //         byte (sign + 7 high exponent bits), the top bytes coded as
-//         (e7 - emin) in k bits plus a sign bit unless the tile's signs agree;
-//         per group of 32 consecutive words: 96 bytes of low bits, then the
-//         codes as b = k + sign bit planes (one 32-bit word per bit)
+//         (e7 - emin) in k bits plus a sign bit unless the tile's signs agree,
+//         packed b = k + sign bits per word
 //   EXPM  MASK's bitmask, then the nonzero words' low bytes (3 each) and their
 //         codes packed b bits each
 // (fp32 activations keep their exponents in a narrow band per tile: k is
@@ -559,9 +558,8 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
     if (mode == kZExpM) {   // the code plane is OR-ed together: clear it (and the padding) first
       for (uint32_t q = hoff / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
       for (uint32_t b = 512u + 3u * (info >> 16) + threadIdx.x; b < hoff; b += 256) chunk[b] = 0;
-    } else if (mode == kZExpD) {   // whole words per 32-word group: only the plane's tail padding
-      const uint32_t used = hoff + 4 * ((nvalid + 31) / 32) * (k + sp);
-      for (uint32_t q = used / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
+    } else if (mode == kZExpD) {   // the low plane is written in whole words; the code plane is OR-ed
+      for (uint32_t q = hoff / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
     }
     if (mode == kZMask || mode == kZExpM) {
 #pragma unroll
@@ -607,10 +605,13 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
         const uint32_t la = __shfl_sync(0xffffffffu, lo, a & 31), lb = __shfl_sync(0xffffffffu, lo, (a + 1) & 31);
         const uint64_t cat = uint64_t(la) | (uint64_t(lb) << 24);
         if (lane < 24) cw[g * 24 + lane] = uint32_t(cat >> (8 * off));
-        const uint32_t code = valid ? ((((v >> 24) & 0x7Fu) - em) | (sp ? (v >> 31) << k : 0u)) : 0u;
-        for (uint32_t q = 0; q < b; ++q) {
-          const uint32_t plane = __ballot_sync(0xffffffffu, (code >> q) & 1u);
-          if (lane == 0) hi[g * b + q] = plane;
+        // codes packed b bits each (the plane was cleared above; two shared-memory
+        // ORs at most per word -- measured faster than warp-wide assembly)
+        if (valid && b) {
+          const uint32_t code = (((v >> 24) & 0x7Fu) - em) | (sp ? (v >> 31) << k : 0u);
+          const uint32_t o = (g * 32 + lane) * b, q = o >> 5, sh = o & 31u;
+          atomicOr(hi + q, code << sh);
+          if (sh + b > 32) atomicOr(hi + q + 1, code >> (32 - sh));
         }
       }
     } else {
@@ -725,12 +726,16 @@ __global__ void __launch_bounds__(256) zvc_decode_kernel(const char* __restrict_
       if (mode == kZRaw) {
         v = cw[j < kZvcTileWords ? j : 0];
       } else if (mode == kZExpD) {
-        // group g = r*8 + warp: its low bytes at 96 g, its code planes at words b g .. b g + b-1
-        const uint32_t g = r * 8 + warp, b = k + sp, sh = (3 * lane & 3) * 8;
-        const uint32_t* lw = cw + g * 24 + (3 * lane) / 4;
+        // word j: low bytes at 3 j (two aligned word loads), code at bit j b (packed)
+        const uint32_t sh = (3 * j & 3) * 8, b = k + sp;
+        const uint32_t* lw = cw + (3 * j) / 4;
         const uint32_t low = ((lw[0] >> sh) | (sh > 8 ? lw[1] << (32 - sh) : 0u)) & 0xFFFFFFu;
         uint32_t code = 0;
-        for (uint32_t q = 0; q < b; ++q) code |= ((hi[g * b + q] >> lane) & 1u) << q;
+        if (b) {
+          const uint32_t o = j * b, q = o >> 5, s2 = o & 31u;
+          code = hi[q] >> s2;
+          if (s2 + b > 32) code |= hi[q + 1] << (32 - s2);
+        }
         const uint32_t e7 = em + (code & ((1u << k) - 1u));
         const uint32_t sg = sp ? (code >> k) & 1u : sc;
         v = i < nwords ? (((sg << 7 | e7) << 24) | low) : 0u;

@@ -161,67 +161,74 @@ class _SavedInfo:
     zx_ratio: float = 1.0
 
 
-def zx_ratio_estimate(t, max_words: int = 1 << 20) -> float:
+def zx_ratio_estimate(t, max_words: int = 1 << 18) -> float:
     """Wire bytes / tensor bytes the ZX codec (ZVC v3 with exponent planes,
     kernels.cuh) would need, computed with the codec's own per-tile rules on
-    the tensor's first ``max_words`` 32-bit words (whole 4096-word tiles)."""
+    the tensor's first ``max_words`` 32-bit words (whole 4096-word tiles; one
+    host copy of the sample, numpy on the host: no per-tensor kernel chain)."""
+    import numpy as np
     if not t.numel() or t.element_size() != 4 or not t.is_contiguous():
         return 1.0
     w = t.detach().reshape(-1).view(torch.int32)
     n = min(w.numel(), max_words) // 4096 * 4096
     if n == 0:
         return 1.0
-    w = w[:n].view(-1, 4096).long() & 0xFFFFFFFF
-    nz = w != 0
-    e7 = (w >> 24) & 0x7F
-    s = w >> 31
+    x = w[:n].cpu().numpy().view(np.uint32).reshape(-1, 4096)
+    nz = x != 0
+    e7 = ((x >> 24) & 0x7F).astype(np.int64)
+    s = (x >> 31).astype(np.int64)
     cnt = nz.sum(1)
 
-    def pad16(x):
-        return (x + 15) // 16 * 16
+    def pad16(v):
+        return (v + 15) // 16 * 16
 
     def bits(r):
-        return torch.where(r > 0, torch.floor(torch.log2(r.clamp(min=1).double())) + 1, torch.zeros_like(r.double()))
+        return np.where(r > 0, np.floor(np.log2(np.maximum(r, 1))) + 1, 0)
 
-    raw = torch.full_like(cnt, 16384).double()
-    mask = (512 + pad16(4 * cnt)).double()
-    kd = bits(e7.max(1).values - e7.min(1).values)
-    sd = (s.max(1).values != s.min(1).values).double()
-    expd = 96 * 128 + pad16(4 * 128 * (kd + sd))
-    big, small = torch.full_like(e7, 127), torch.zeros_like(e7)
-    km = bits(torch.where(nz, e7, small).max(1).values - torch.where(nz, e7, big).min(1).values)
-    sm = (torch.where(nz, s, small).max(1).values != torch.where(nz, s, torch.ones_like(s)).min(1).values).double()
-    expm = 512 + pad16(3 * cnt).double() + pad16(torch.ceil(cnt * (km + sm) / 8))
-    expm = torch.where(cnt > 0, expm, mask)
-    best = torch.minimum(torch.minimum(raw, mask), torch.minimum(expd, expm))
-    return float((best.sum() + 8 * best.numel()) / (4.0 * n))
+    raw = np.full(cnt.shape, 16384.0)
+    mask = 512.0 + pad16(4 * cnt)
+    kd = bits(e7.max(1) - e7.min(1))
+    sd = (s.max(1) != s.min(1)).astype(np.float64)
+    expd = 96.0 * 128 + pad16(4 * 128 * (kd + sd))
+    km = bits(np.where(nz, e7, 0).max(1) - np.where(nz, e7, 127).min(1))
+    sm = (np.where(nz, s, 0).max(1) != np.where(nz, s, 1).min(1)).astype(np.float64)
+    expm = np.where(cnt > 0, 512.0 + pad16(3 * cnt) + pad16(np.ceil(cnt * (km + sm) / 8)), mask)
+    best = np.minimum(np.minimum(raw, mask), np.minimum(expd, expm))
+    return float((best.sum() + 8 * best.size) / (4.0 * n))
 
 
 class _Capture:
     """Records packs (forward) and consumers (backward) for one traced step."""
 
-    def __init__(self):
+    def __init__(self, min_bytes: int = 0):
         self.packs = []        # pack idx -> (tensor key, nbytes, grad_fn or None, is_leaf, requires_grad)
         self.keep = []         # strong refs so addresses stay unique during capture
         self.consumer = {}     # pack idx -> autograd node that unpacked it
         self.zero_frac = []    # pack idx -> share of zero words (capture-time contents)
         self.zx_ratio = []     # pack idx -> ZX codec wire/tensor bytes (capture-time contents)
+        self.min_bytes = min_bytes   # smaller tensors are never swap candidates: not measured
+        self._measured = {}    # tensor key -> (zero_frac, zx_ratio): a tensor saved twice is measured once
 
     def pack(self, t):
         k = len(self.packs)
         key = (t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype)
-        self.packs.append((key, t.numel() * t.element_size(), t.grad_fn, t.is_leaf,
-                           t.requires_grad, isinstance(t, torch.nn.Parameter)))
-        # share of all-zero 32-bit words: what the ZVC codec would drop
-        zf = 0.0
-        if (t.numel() and t.element_size() == 4 and t.is_contiguous()
-                and not isinstance(t, torch.nn.Parameter)):
-            w = t.detach().view(-1).view(torch.int32)
-            if w.numel() > (1 << 22):      # a strided sample: no tensor-sized temporaries
-                w = w[:: w.numel() >> 22]
-            zf = 1.0 - float(torch.count_nonzero(w)) / w.numel()
-        self.zero_frac.append(zf)
-        self.zx_ratio.append(zx_ratio_estimate(t) if not isinstance(t, torch.nn.Parameter) else 1.0)
+        nbytes = t.numel() * t.element_size()
+        is_param = isinstance(t, torch.nn.Parameter)
+        self.packs.append((key, nbytes, t.grad_fn, t.is_leaf, t.requires_grad, is_param))
+        m = self._measured.get(key)
+        if m is None:
+            # share of all-zero 32-bit words, and the ZX codec's stream ratio
+            zf, zx = 0.0, 1.0
+            if (nbytes >= self.min_bytes and t.numel() and t.element_size() == 4 and t.is_contiguous()
+                    and not is_param):
+                w = t.detach().view(-1).view(torch.int32)
+                if w.numel() > (1 << 22):      # a strided sample: no tensor-sized temporaries
+                    w = w[:: w.numel() >> 22]
+                zf = 1.0 - float(torch.count_nonzero(w)) / w.numel()
+                zx = zx_ratio_estimate(t)
+            m = self._measured[key] = (zf, zx)
+        self.zero_frac.append(m[0])
+        self.zx_ratio.append(m[1])
         t = t.detach()   # no tensor -> grad_fn -> saved -> tensor cycle (see SwapExecutor.pack)
         self.keep.append(t)
         return (k, t)
@@ -267,7 +274,7 @@ def capture_graph(forward_fn, min_swap_bytes: int = 1 << 16, persistent=()):
     place.
     """
     keep_ptrs = {t.data_ptr() for t in persistent if t is not None and t.numel()}
-    cap = _Capture()
+    cap = _Capture(min_swap_bytes)
     sizes = _OutputBytes()
     with torch.autograd.graph.saved_tensors_hooks(cap.pack, cap.unpack), sizes:
         loss = forward_fn()

@@ -151,7 +151,7 @@ def main():
     ev = [{"name": "forward", "ph": "X", "pid": 0, "tid": 0, "ts": 0.0, "dur": (tf - t0) * 1e3},
           {"name": "backward+optimizer", "ph": "X", "pid": 0, "tid": 0, "ts": (tf - t0) * 1e3,
            "dur": (te - tf) * 1e3}]
-    names = {0: "copy-engine", 1: "sm-zero-copy", 2: "zvc"}
+    names = {0: "copy-engine", 1: "sm-zero-copy", 2: "zvc", 3: "zx"}
     for r in tr:
         ev.append({"name": f"{'swap-out' if r['direction'] == 0 else 'swap-in'} {names.get(r['codec'])} "
                            f"{r['logical_bytes'] / 2**20:.0f} MiB -> {r['wire_bytes'] / 2**20:.0f} MiB",
