@@ -1133,6 +1133,37 @@ class LMS:
                 "steps_per_trial": steps, "peak_before": start_peak,
                 "limit": limit, "lower_bound": info["lower_bound_bytes"]}
 
+    def plan_by_model(self, x, y, cfgs, batch: int, link, budget_bytes: int, capture_batch: int = 4):
+        """Rank candidate ``RewriteConfig``s by the calibrated model (calibrate.py):
+        one plain step at (x, y) — a batch that fits without swapping — is timed
+        per captured node and gives the fixed (non-activation) bytes; costs and
+        tensor sizes are scaled to ``batch``; each config's rewrite of the
+        captured graph is predicted.  Returns ``[(cfg, prediction, fits)]``,
+        fitting configs fastest first.  The model's parameters move by one
+        optimizer step (like ``autotune``)."""
+        from . import calibrate as cal
+        b = x.shape[0]
+        torch.cuda.synchronize()
+        self.ctx.reset_peaks()
+        live0 = self.ctx.stats()["device_in_use"]
+        costs = cal.node_costs(self.model, self.loss_fn, x, y, self.meta, self.optimizer)
+        plain_peak = self.ctx.stats()["device_peak"] - live0
+        g_b = cal.calibrated_graph(self.graph, costs, b / capture_batch, 1.0, costs["_optimizer_total"])
+        fixed = plain_peak - cal.predict(g_b, link)["peak_device_bytes"]
+        g_t = cal.calibrated_graph(self.graph, costs, batch / capture_batch, batch / b, costs["_optimizer_total"])
+        self.model_costs, self.model_fixed_bytes = costs, fixed
+        return cal.plan_ranking(g_t, cfgs, link, budget_bytes - fixed)
+
+    def link_model(self, link_gbs: dict, zc_efficiency: float = 0.9):
+        """A ``calibrate.LinkModel`` from measured copy-engine rates (GB/s, bench's
+        ``measure_host_link``) and the capture step's per-tensor ZX ratios."""
+        from .calibrate import LinkModel
+        wire = {self.meta["saved_tensor_id"][s.tid]: s.zx_ratio for s in self.meta["saved"]
+                if s.tid in self.meta["saved_tensor_id"]}
+        return LinkModel(d2h_ce=link_gbs["d2h"] * 1e9, h2d_ce=link_gbs["h2d"] * 1e9,
+                         d2h_zc=zc_efficiency * link_gbs["d2h"] * 1e9, h2d_zc=zc_efficiency * link_gbs["h2d"] * 1e9,
+                         wire_ratio=wire, zx_max_ratio=SwapExecutor.ZX_MAX_RATIO)
+
     def _set_plan(self, plan: SwapPlan):
         self.plan = plan
         self._exec = SwapExecutor(self.ctx, plan, self.codec)
