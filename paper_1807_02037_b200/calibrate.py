@@ -18,10 +18,13 @@ a real run.  Here they come from measurements on the B200:
   executor: ops in the serial (order, id) sequence on one compute stream,
   swap-outs and swap-ins in issue order on their copy channels (one shared
   channel without overlap), each swap-in gated by its control op and its
-  swap-out — the same gating the GPU executor uses — and reports the
-  makespan, the link busy time and the activation peak (tensors allocated at
-  their producer's start, released after their last reader, a swapped tensor
-  only after its copy landed: sim.py:205-211);
+  swap-out — the same gating the GPU executor uses — with allocations
+  throttled by the room the budget leaves (an op waits for already-known
+  frees, as the pool makes it wait for swap-out copies); it reports the
+  makespan, the link busy time, the allocation stalls, the activation peak
+  and whether the step fits (tensors allocated at their producer's start,
+  released after their last reader, a swapped tensor only after its copy
+  landed: sim.py:205-211);
 * ``LMS.plan_by_model`` ranks candidate ``RewriteConfig``s by predicted step
   time among those whose predicted peak fits the budget.
 
@@ -143,8 +146,27 @@ def node_costs(model, loss_fn, x, y, meta: dict, optimizer=None) -> dict[int, fl
 
 
 def calibrated_graph(g: CompGraph, costs: dict, size_scale: float, cost_scale: float = 1.0,
-                     update_total: float = 0.0) -> CompGraph:
-    """``g`` with measured ``cost_hint`` seconds (x cost_scale) and tensor sizes x size_scale."""
+                     update_total: float = 0.0, meta: dict | None = None) -> CompGraph:
+    """``g`` with measured ``cost_hint`` seconds (x cost_scale) and tensor sizes x size_scale.
+
+    With the capture's ``meta``, the backward ops' gradient tensors (sized 0 by
+    the capture: autograd does not save them) get the size of the forward
+    outputs they are the gradients of, so the model sees backward memory."""
+    if meta is not None:
+        F_of_rank = {r: nid for nid, r in meta["F"].items()}
+        main_out = {}
+        for t in g.tensors:
+            if t.producer in meta["F"] and t.producer not in main_out:
+                main_out[t.producer] = t.size_bytes     # the F node's first tensor: its output
+        sized = []
+        for t in g.tensors:
+            if t.size_bytes == 0 and t.producer in meta["B"]:
+                # consumers B(m): this tensor carries the gradient of m's forward output
+                ranks = {meta["B"][e.dst] for e in g.consumer_edges(t.id) if e.dst in meta["B"]}
+                nb = sum(main_out.get(F_of_rank.get(r), 0) for r in ranks)
+                t = TensorSpec(t.id, t.producer, nb, t.dtype)
+            sized.append(t)
+        g = CompGraph(list(g.nodes), list(g.edges), sized)
     upd = [n.id for n in g.nodes if n.phase.value == "update"]
     per_upd = update_total * cost_scale / max(1, len(upd))
     nodes = []
@@ -180,8 +202,17 @@ class LinkModel:
         return 1.0, self.d2h_ce if d2h else self.h2d_ce
 
 
-def predict(g: CompGraph, link: LinkModel, order: dict | None = None) -> dict:
-    """List-scheduling model of one step of rewritten graph ``g`` (see module doc)."""
+def predict(g: CompGraph, link: LinkModel, order: dict | None = None, room_bytes: float = float("inf")) -> dict:
+    """List-scheduling model of one step of rewritten graph ``g`` (see module doc).
+
+    Memory is throttled like the pool throttles it: an op (or a swap-in's
+    destination) that would take the live activations past ``room_bytes``
+    waits until enough already-scheduled frees have happened — a tensor is
+    released once all its readers finished, a swapped tensor only after its
+    copy landed (sim.py:205-211).  ``fits`` is False when no pending free can
+    make room (the real pool would raise LMS_OOM)."""
+    import heapq
+
     order = order or topo_order(g)
     ex = _exec_set(g)
     seq = _schedule(g, order, ex)
@@ -196,66 +227,102 @@ def predict(g: CompGraph, link: LinkModel, order: dict | None = None) -> dict:
             cur = ins[0].tensor
         return cur
 
+    # readers per device-resident tensor (swap-outs read their source too)
+    left, last = {}, {}
+    for nid in seq:
+        for e in g.in_edges(nid):
+            if e.action is EdgeAction.READ and not nbi[tbi[e.tensor].producer].parameterized:
+                left[e.tensor] = left.get(e.tensor, 0) + 1
+    frees: list[tuple[float, int]] = []     # (time, bytes) of releases already known
+    live = peak = 0
+    fits = True
+    stall = 0.0
+
+    def make_room(t, need):
+        """Earliest time >= t at which need bytes fit (pops the frees that happened).
+        Queried on the compute stream's timeline only, which never goes back."""
+        nonlocal live, fits, stall
+        while frees and frees[0][0] <= t:
+            live -= heapq.heappop(frees)[1]
+        t_in = t
+        while live + need > room_bytes:
+            if not frees:
+                fits = False
+                break
+            ft, b = heapq.heappop(frees)
+            t = max(t, ft)
+            live -= b
+        stall += t - t_in
+        return t
+
     start, finish = {}, {}
     engine = d2h = h2d = 0.0
     busy = {"d2h": 0.0, "h2d": 0.0}
     for nid in seq:
         node = nbi[nid]
         ready = 0.0
+        reads = []
         for e in g.in_edges(nid):
             if e.action is EdgeAction.READ and not nbi[tbi[e.tensor].producer].parameterized:
                 ready = max(ready, finish[tbi[e.tensor].producer])
+                reads.append(e.tensor)
             elif e.action is EdgeAction.CONTROL and e.src in finish:
                 ready = max(ready, finish[e.src])
+        outs = [t for t in g.produced_tensors(nid) if t.size_bytes > 0]
+        need = 0 if node.kind is NodeKind.SWAP_OUT else sum(t.size_bytes for t in outs)
         if node.kind is NodeKind.SWAP_OUT or node.kind is NodeKind.SWAP_IN:
             out_dir = node.kind is NodeKind.SWAP_OUT
-            src = next(e.tensor for e in g.in_edges(nid) if e.action is EdgeAction.READ)
+            src = reads[0]
             ratio, bw = link.rate(origin(src), out_dir)
             dur = tbi[src].size_bytes * ratio / bw
+            ch = d2h if (out_dir or not link.overlap) else h2d
+            if out_dir:
+                t0 = max(ch, ready)
+            else:
+                # the destination is allocated on the issuing (compute) thread, which
+                # the pool blocks until the room is there; without a stall the H2D
+                # starts when its control op (and swap-out) completed
+                t_room = make_room(engine, need)
+                stalled = t_room > engine
+                engine = max(engine, t_room)
+                t0 = max(ch, ready, t_room if stalled else 0.0)
             if out_dir or not link.overlap:
-                t0 = max(d2h, ready)
                 d2h = t0 + dur
                 if not link.overlap:
                     h2d = d2h
             else:
-                t0 = max(h2d, ready)
                 h2d = t0 + dur
             busy["d2h" if out_dir else "h2d"] += dur
-            start[nid], finish[nid] = t0, t0 + dur
         else:
-            t0 = max(engine, ready)
-            engine = t0 + node.cost_hint
-            start[nid], finish[nid] = t0, engine
-    # activation residency: from the producer's start to the last reader's finish
-    # (a swap-out reader holds its source until the copy lands, sim.py:205-211)
-    delta: list[tuple[float, int]] = []
-    for t in g.tensors:
-        p = nbi[t.producer]
-        if t.producer not in start or t.size_bytes <= 0 or p.kind is NodeKind.SWAP_OUT:
-            continue
-        readers = [finish[e.dst] for e in g.consumer_edges(t.id) if e.action is EdgeAction.READ and e.dst in finish]
-        end = max(readers, default=finish[t.producer])
-        delta.append((start[t.producer], t.size_bytes))
-        delta.append((end, -t.size_bytes))
-    delta.sort(key=lambda d: (d[0], d[1]))
-    live = peak = 0
-    for _, b in delta:
-        live += b
+            t0 = make_room(max(engine, ready), need)
+            dur = node.cost_hint
+            engine = t0 + dur
+        start[nid], finish[nid] = t0, t0 + dur
+        live += need
         peak = max(peak, live)
+        for tid in reads:
+            last[tid] = max(last.get(tid, 0.0), finish[nid])
+            left[tid] -= 1
+            if left[tid] == 0:
+                heapq.heappush(frees, (last[tid], tbi[tid].size_bytes))
+        for t in outs:
+            if node.kind is not NodeKind.SWAP_OUT and left.get(t.id, 0) == 0:
+                heapq.heappush(frees, (finish[nid], t.size_bytes))   # only update edges read it
     makespan = max(finish.values(), default=0.0)
-    return {"makespan": makespan, "peak_device_bytes": peak, "d2h_busy": busy["d2h"], "h2d_busy": busy["h2d"],
+    return {"makespan": makespan, "peak_device_bytes": peak, "fits": fits, "alloc_stall": stall,
+            "d2h_busy": busy["d2h"], "h2d_busy": busy["h2d"],
             "compute": sum(nbi[n].cost_hint for n in seq
                            if nbi[n].kind not in (NodeKind.SWAP_OUT, NodeKind.SWAP_IN))}
 
 
 def plan_ranking(graph: CompGraph, cfgs, link: LinkModel, room_bytes: float):
-    """Each config's predicted step; those whose activation peak fits ``room_bytes``
-    come first, fastest first.  Returns [(cfg, prediction, fits)]."""
+    """Each config's predicted step under ``room_bytes`` of activation memory;
+    those that fit come first, fastest first.  Returns [(cfg, prediction, fits)]."""
     from .rewriter import rewrite
     out = []
     for cfg in cfgs:
         g2, _ = rewrite(graph, cfg)
-        p = predict(g2, link)
-        out.append((cfg, p, p["peak_device_bytes"] <= room_bytes))
+        p = predict(g2, link, room_bytes=room_bytes)
+        out.append((cfg, p, p["fits"]))
     out.sort(key=lambda c: (not c[2], c[1]["makespan"]))
     return out

@@ -1148,9 +1148,10 @@ class LMS:
         live0 = self.ctx.stats()["device_in_use"]
         costs = cal.node_costs(self.model, self.loss_fn, x, y, self.meta, self.optimizer)
         plain_peak = self.ctx.stats()["device_peak"] - live0
-        g_b = cal.calibrated_graph(self.graph, costs, b / capture_batch, 1.0, costs["_optimizer_total"])
+        g_b = cal.calibrated_graph(self.graph, costs, b / capture_batch, 1.0, costs["_optimizer_total"], self.meta)
         fixed = plain_peak - cal.predict(g_b, link)["peak_device_bytes"]
-        g_t = cal.calibrated_graph(self.graph, costs, batch / capture_batch, batch / b, costs["_optimizer_total"])
+        g_t = cal.calibrated_graph(self.graph, costs, batch / capture_batch, batch / b, costs["_optimizer_total"],
+                                   self.meta)
         self.model_costs, self.model_fixed_bytes = costs, fixed
         return cal.plan_ranking(g_t, cfgs, link, budget_bytes - fixed)
 

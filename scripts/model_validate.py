@@ -127,7 +127,8 @@ def main():
             ctx.synchronize()
         rows.append({"lb": cfg.lb, "n_tensors": cfg.n_tensors, "predicted_ms": round(pred["makespan"] * 1e3, 1),
                      "predicted_peak_gib": round((pred["peak_device_bytes"] + fixed) / GIB, 2),
-                     "predicted_fits": fit, "measured_ms": None if ms is None else round(ms, 1)})
+                     "predicted_fits": fit, "predicted_alloc_stall_ms": round(pred["alloc_stall"] * 1e3, 1),
+                     "measured_ms": None if ms is None else round(ms, 1)})
         print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
     both = [r for r in rows if r["measured_ms"] is not None]
     out = {"arch": a.arch, "b0": b0, "batch": bs, "budget_gib": a.budget_gib,

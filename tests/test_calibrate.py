@@ -44,10 +44,13 @@ def test_wider_windows_trade_memory_for_time():
     preds = {c.lb: p for c, p, _ in plan_ranking(g, cfgs, link, 1e18)}
     assert preds[8]["makespan"] < preds[2]["makespan"] < preds[1]["makespan"]
     assert preds[16]["peak_device_bytes"] > preds[1]["peak_device_bytes"]
-    # a room below lb 16's peak ranks it behind every config that fits
-    ranked = plan_ranking(g, cfgs, link, preds[1]["peak_device_bytes"])
-    assert [c.lb for c, _, fit in ranked if not fit] == [16]
-    assert ranked[0][0].lb == 8
+    # a tight room: allocations wait for swap-out copies (the pool's throttle), the
+    # peak stays under the room, and a room below one op's working set does not fit
+    tight = {c.lb: (p, fit) for c, p, fit in plan_ranking(g, cfgs, link, 4 << 20)}
+    for lb, (p, fit) in tight.items():
+        assert fit and p["peak_device_bytes"] <= 4 << 20 and p["alloc_stall"] > 0
+        assert p["makespan"] >= preds[lb]["makespan"]
+    assert not any(fit for _, _, fit in plan_ranking(g, cfgs, link, 1 << 20))
 
 
 def test_wire_ratio_shortens_transfers():
