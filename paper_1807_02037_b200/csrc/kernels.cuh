@@ -409,9 +409,7 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
                                                             char* __restrict__ out, int use_bulk) {
   constexpr int allow_exp = kExp;
   extern __shared__ __align__(128) unsigned char zsm[];
-  __shared__ uint32_t seg[kZvcMaskWords + 1];
   __shared__ uint32_t red[8][9];
-  __shared__ uint32_t pick[3];   // info, bytes, hi-plane offset
   const uint64_t ntiles = zvc_tiles(nwords);
   const uint64_t dpos = zvc_data_pos(ntiles);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -523,57 +521,67 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
       red[warp][5] = mn_z; red[warp][6] = mx_z; red[warp][7] = or_z; red[warp][8] = and_z;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int k = 1; k < 8; ++k) {
-        red[0][0] += red[k][0];
-        red[0][1] = min(red[0][1], red[k][1]); red[0][2] = max(red[0][2], red[k][2]);
-        red[0][3] |= red[k][3]; red[0][4] &= red[k][4];
-        red[0][5] = min(red[0][5], red[k][5]); red[0][6] = max(red[0][6], red[k][6]);
-        red[0][7] |= red[k][7]; red[0][8] &= red[k][8];
+    // every thread takes the same decision from the 8 warps' partials (no
+    // serial thread-0 step, no second barrier)
+    uint32_t z = 0, mna = 127, mxa = 0, ora = 0, anda = 1, mnz = 127, mxz = 0, orz = 0, andz = 1;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      z += red[k][0];
+      if (kExp) {
+        mna = min(mna, red[k][1]); mxa = max(mxa, red[k][2]); ora |= red[k][3]; anda &= red[k][4];
+        mnz = min(mnz, red[k][5]); mxz = max(mxz, red[k][6]); orz |= red[k][7]; andz &= red[k][8];
       }
-      const uint32_t z = red[0][0];
-      uint32_t mode = kZRaw, bytes = zvc_pad16(4ull * nvalid), n = nvalid, k = 0, sp = 0, sc = 0, em = 0, hoff = 0;
+    }
+    uint32_t mode = kZRaw, bytes = zvc_pad16(4ull * nvalid), n = nvalid, k = 0, sp = 0, sc = 0, em = 0, hoff = 0;
+    {
       const uint32_t bm = 512 + zvc_pad16(4ull * z);
       if (bm < bytes) mode = kZMask, bytes = bm, n = z;
-      if (allow_exp) {
-        const uint32_t kd = zvc_nbits(red[0][2] - red[0][1]), sd = red[0][3] != red[0][4];
+      if (kExp) {
+        const uint32_t kd = zvc_nbits(mxa - mna), sd = ora != anda;
         const uint32_t ng = (nvalid + 31) / 32;
         const uint32_t bd = 96 * ng + zvc_pad16(4ull * ng * (kd + sd));
-        if (bd < bytes) mode = kZExpD, bytes = bd, n = nvalid, k = kd, sp = sd, sc = red[0][3], em = red[0][1],
-                        hoff = 96 * ng;
+        if (bd < bytes) mode = kZExpD, bytes = bd, n = nvalid, k = kd, sp = sd, sc = ora, em = mna, hoff = 96 * ng;
         if (z) {
-          const uint32_t km = zvc_nbits(red[0][6] - red[0][5]), sm = red[0][7] != red[0][8];
+          const uint32_t km = zvc_nbits(mxz - mnz), sm = orz != andz;
           const uint32_t be = 512 + zvc_pad16(3ull * z) + zvc_pad16((uint64_t(z) * (km + sm) + 7) / 8);
-          if (be < bytes) mode = kZExpM, bytes = be, n = z, k = km, sp = sm, sc = red[0][7], em = red[0][5],
+          if (be < bytes) mode = kZExpM, bytes = be, n = z, k = km, sp = sm, sc = orz, em = mnz,
                           hoff = 512 + zvc_pad16(3ull * z);
         }
       }
-      pick[0] = mode | k << 2 | sp << 6 | sc << 7 | em << 8 | n << 16;
-      pick[1] = bytes;
-      pick[2] = hoff;
     }
-    __syncthreads();
-    const uint32_t info = pick[0], bytes = pick[1], hoff = pick[2];
-    const uint32_t mode = info & 3u, k = (info >> 2) & 15u, sp = (info >> 6) & 1u, em = (info >> 8) & 0x7Fu;
+    const uint32_t info = mode | k << 2 | sp << 6 | sc << 7 | em << 8 | n << 16;
     if (mode == kZExpM) {   // the code plane is OR-ed together: clear it (and the padding) first
       for (uint32_t q = hoff / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
-      for (uint32_t b = 512u + 3u * (info >> 16) + threadIdx.x; b < hoff; b += 256) chunk[b] = 0;
+      for (uint32_t b = 512u + 3u * n + threadIdx.x; b < hoff; b += 256) chunk[b] = 0;
     } else if (mode == kZExpD) {   // the low plane is written in whole words; the code plane is OR-ed
       for (uint32_t q = hoff / 4 + threadIdx.x; q < bytes / 4; q += 256) cw[q] = 0u;
     }
-    if (mode == kZMask || mode == kZExpM) {
+    const bool masked = mode == kZMask || mode == kZExpM;
+    if (masked) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const uint32_t m = __ballot_sync(0xffffffffu, w16[r] != 0);
-        if (lane == 0) {
-          cw[r * 8 + warp] = m;
-          seg[r * 8 + warp] = __popc(m);
-        }
+        if (lane == 0) cw[r * 8 + warp] = m;
       }
-      __syncthreads();
-      if (warp == 0) zvc_seg_scan(seg, lane);
     }
-    __syncthreads();
+    if (mode != kZRaw) __syncthreads();   // masks complete, planes cleared
+    // masked forms: each warp scans the 128 mask popcounts itself; the prefix of
+    // mask word r*8 + warp sits in lane 2r + warp/4 at position warp % 4
+    uint32_t psel = 0;
+    if (masked) {
+      const uint32_t c0 = __popc(cw[4 * lane]), c1 = __popc(cw[4 * lane + 1]);
+      const uint32_t c2 = __popc(cw[4 * lane + 2]), c3 = __popc(cw[4 * lane + 3]);
+      const uint32_t sum = c0 + c1 + c2 + c3;
+      uint32_t x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t ex = x - sum;
+      const uint32_t pos = warp & 3;
+      psel = ex + (pos > 0 ? c0 : 0) + (pos > 1 ? c1 : 0) + (pos > 2 ? c2 : 0);
+    }
     if (mode == kZRaw) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -584,9 +592,9 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const uint32_t m = cw[r * 8 + warp];
-        if (w16[r] != 0) cw[kZvcMaskWords + seg[r * 8 + warp] + __popc(m & lt)] = w16[r];
+        const uint32_t base_r = __shfl_sync(0xffffffffu, psel, 2 * r + (warp >> 2));
+        if (w16[r] != 0) cw[kZvcMaskWords + base_r + __popc(m & lt)] = w16[r];
       }
-      const uint32_t z = seg[kZvcMaskWords];
       if (threadIdx.x < ((z + 3) & ~3u) - z) cw[kZvcMaskWords + z + threadIdx.x] = 0u;
     } else if (mode == kZExpD) {
       // warp-cooperative: a warp's 32 consecutive words are one group -- their low
@@ -619,7 +627,8 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const uint32_t m = cw[r * 8 + warp];
-        if (w16[r] != 0) zvc_put_exp(chunk + 512, hi, seg[r * 8 + warp] + __popc(m & lt), w16[r], k, sp, em);
+        const uint32_t base_r = __shfl_sync(0xffffffffu, psel, 2 * r + (warp >> 2));
+        if (w16[r] != 0) zvc_put_exp(chunk + 512, hi, base_r + __popc(m & lt), w16[r], k, sp, em);
       }
     }
     char* dst = data + t * kZvcSlotBytes;
