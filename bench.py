@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--tf32", action="store_true")
     ap.add_argument("--same-batch", type=int, default=1,
                     help="also time TFLMS (every candidate swapped) at B0 against the plain step at B0")
+    ap.add_argument("--model-select", action="store_true",
+                    help="pick lb by the calibrated model (calibrate.py: per-node times of a plain step at B0, "
+                         "the run's link rates) instead of the default lb")
     ap.add_argument("--autotune", action="store_true",
                     help="pick lb empirically (LMS.autotune over 1,2,3,5,8) before the timed run")
     ap.add_argument("--tune-windows", type=int, default=2,
@@ -210,7 +213,7 @@ def main():
 
     import torch
     import torchvision
-    from paper_1807_02037_b200 import RewriteConfig, runtime as rt
+    from paper_1807_02037_b200 import RewriteConfig, rewrite as rewrite_fn, runtime as rt
     from paper_1807_02037_b200.torch_lms import LMS
 
     if not torch.cuda.is_available():
@@ -401,6 +404,42 @@ def main():
     plan = lms.capture(xc, yc)
     capture_s = time.perf_counter() - t_cap
     xc = yc = None
+    # the calibrated model (calibrate.py): one plain step at B0 timed per node
+    # predicts each window at the swapped batch; reported next to the measured
+    # step, and with --model-select it picks lb
+    model_info = None
+    bs_target = args.batch or max(1, int(math.ceil(args.factor * b0)))
+    if b0 > 0 and not use_dist:
+        try:
+            xm, ym = batch(b0, seed=5)
+            lm = lms.link_model(link)
+            lbs = (1, 2, 3, 5, 8)
+            cfgs = [RewriteConfig(lb=lb, ub=max(args.ub, lb), ctrld_strategy=args.strategy,
+                                  swap_branches=args.branches, branch_threshold=args.branch_threshold,
+                                  fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance)
+                    for lb in lbs]
+            ranked = lms.plan_by_model(xm, ym, cfgs, bs_target, lm, budget, capture_batch=cap_b / cap_scale
+                                       if args.arch == "unet3d" else cap_b)
+            model_info = {"calibration_batch": b0, "target_batch": bs_target,
+                          "fixed_bytes": int(lms.model_fixed_bytes),
+                          "candidates": [{"lb": c.lb, "predicted_ms": round(p["makespan"] * 1e3, 1),
+                                          "predicted_alloc_stall_ms": round(p["alloc_stall"] * 1e3, 1),
+                                          "fits": fit} for c, p, fit in ranked]}
+            if args.model_select and ranked and ranked[0][2]:
+                args.lb = ranked[0][0].lb
+                model_info["selected_lb"] = args.lb
+            log(f"[bench] model: {model_info['candidates']}")
+        except RuntimeError as e:
+            if not is_oom(e):
+                raise
+            traceback.clear_frames(e.__traceback__)
+            model_info = {"error": str(e)[:200]}
+        xm = ym = None
+        opt.zero_grad(set_to_none=True)
+        gc.collect()
+        torch.cuda.synchronize(dev)
+        ctx.synchronize()
+
     # candidate tensors in the rewrite's BFS order with their per-image bytes
     order = []
     seen = set()
@@ -657,6 +696,16 @@ def main():
         raise SystemExit("swapped run did not fit the budget")
     plan = lms.plan
     log(f"[bench] plan: {plan.summary()}")
+    if model_info and "candidates" in model_info:
+        # the model's prediction for the configuration that was timed (its untuned
+        # windows: the tuner's per-swap-in moves are not in the rewrite's graph)
+        from paper_1807_02037_b200.calibrate import predict
+        g_timed, _ = rewrite_fn(lms.model_graph, lms.cfg)
+        p_t = predict(g_timed, lms.link_model(link), room_bytes=lms.model_room)
+        model_info["timed_config"] = {"lb": lms.cfg.lb, "n_tensors": plan.report.tensors_swapped,
+                                      "predicted_ms": round(p_t["makespan"] * 1e3, 1),
+                                      "measured_untuned_ms": (tuned or {}).get("base_ms"),
+                                      "measured_ms": round(swap_ms / args.steps, 1)}
     st1 = ctx.stats()
     trace = ctx.trace()
     value = bs * ws * args.steps / (swap_ms * 1e-3)
@@ -815,6 +864,7 @@ def main():
                 "d2h_bytes_per_step": 4},
         "gpu_launches": kernels,
         "step_ms": STEP_MS,
+        "model": model_info,
         "clocks": clk,
     }
     if rank == 0:

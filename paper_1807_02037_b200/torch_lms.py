@@ -1152,7 +1152,8 @@ class LMS:
         fixed = plain_peak - cal.predict(g_b, link)["peak_device_bytes"]
         g_t = cal.calibrated_graph(self.graph, costs, batch / capture_batch, batch / b, costs["_optimizer_total"],
                                    self.meta)
-        self.model_costs, self.model_fixed_bytes = costs, fixed
+        self.model_costs, self.model_fixed_bytes, self.model_graph = costs, fixed, g_t
+        self.model_room = budget_bytes - fixed
         return cal.plan_ranking(g_t, cfgs, link, budget_bytes - fixed)
 
     def link_model(self, link_gbs: dict, zc_efficiency: float = 0.9):
