@@ -695,7 +695,7 @@ class _ForwardSwaps(TorchFunctionMode):
         kwargs = kwargs or {}
         if self.freed:
             for a in tree_flatten((args, kwargs))[0]:
-                if isinstance(a, torch.Tensor):
+                if isinstance(a, torch.Tensor) and a.layout == torch.strided:
                     tid = self.freed.get(a.untyped_storage()._cdata)
                     if tid is not None:
                         x = self.state[tid]
