@@ -46,16 +46,20 @@ def main():
         json.dump(rows, fh)
     lines = [f"# {a.arch}: swap overhead vs oversubscription under {a.budget_gib:g} GiB {a.extra}", "",
              "overhead = (no-swap img/s at B0) / (swapped img/s at f x B0) - 1, per image", "",
-             "| f | batch | tensors swapped / candidates | img/s | ms/step | D2H GB | overhead |",
-             "|---|---|---|---|---|---|---|"]
+             "| f | batch | tensors swapped | img/s | ms/step | D2H GB | overhead | tuner trial ms | timed / trial |",
+             "|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         if "error" in r:
             lines.append(f"| {r['factor']} | error: {r['error']} | | | | | |")
             continue
         s, ns = r["swap"], r["no_swap"]
         ov = ns["img_s"] / r["value"] - 1
+        tw = s.get("tune_windows") or {}
+        trial = tw.get("final_ms") or (tw.get("trials") or {}).get(str(tw.get("moved"))) or tw.get("base_ms")
+        ratio = f"{r['ms_per_step'] / trial:.3f}" if trial else "-"
         lines.append(f"| {r['factor']} | {r['config']['per_gpu_batch']} | {s['tensors_swapped']} | {r['value']} | "
-                     f"{r['ms_per_step']} | {s['d2h_bytes_per_step'] / 1e9:.1f} | {ov:+.1%} |")
+                     f"{r['ms_per_step']} | {s['d2h_bytes_per_step'] / 1e9:.1f} | {ov:+.1%} | "
+                     f"{round(trial, 1) if trial else '-'} | {ratio} |")
     md = "\n".join(lines) + "\n"
     with open(os.path.join(ROOT, "gpurun_out", f"overhead_{a.arch}{a.tag}.md"), "w") as fh:
         fh.write(md)
