@@ -396,13 +396,19 @@ def main():
                          fuse_swapins=args.fuse_swapins, swapin_fuse_distance=args.fuse_distance)
     codec = args.codec
     # tensors under 64 KiB at the capture size stay on the device
+    from paper_1807_02037_b200.torch_lms import SwapExecutor
     if args.zx_max_ratio > 0:
-        from paper_1807_02037_b200.torch_lms import SwapExecutor
         SwapExecutor.ZX_MAX_RATIO = args.zx_max_ratio
     lms = LMS(model, loss_fn, opt, cfg0, ctx, codec=codec, min_swap_bytes=64 << 10)
     t_cap = time.perf_counter()
     plan = lms.capture(xc, yc)
     capture_s = time.perf_counter() - t_cap
+    bs_planned = args.batch or max(1, int(math.ceil(args.factor * b0)))
+    if noswap_ms and b0 and not args.zx_max_ratio and link.get("d2h"):
+        # auto codec: each plan's swap traffic against the compute it can hide behind
+        # (the no-swap step scaled to the swapped batch): SwapExecutor.zx_policy
+        lms.set_link_context(link["d2h"], noswap_ms / args.steps * 1e-3 * bs_planned / b0,
+                             bs_planned * cap_scale)
     xc = yc = None
     # the calibrated model (calibrate.py): one plain step at B0 timed per node
     # predicts each window at the swapped batch; reported next to the measured
@@ -865,6 +871,10 @@ def main():
         "gpu_launches": kernels,
         "step_ms": STEP_MS,
         "model": model_info,
+        "codec_policy": {"zx_max_ratio": lms._exec.zx_max_ratio,
+                         "link_s": round(plan.swapped_bytes_per_step * lms.link_context[2] /
+                                         (lms.link_context[0] * 1e9), 3) if lms.link_context else None,
+                         "compute_s": round(lms.link_context[1], 3) if lms.link_context else None},
         "clocks": clk,
     }
     if rank == 0:

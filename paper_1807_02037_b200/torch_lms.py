@@ -745,10 +745,11 @@ class _SwapRef:
 class SwapExecutor:
     """Runs training steps under a :class:`SwapPlan` on one device."""
 
-    def __init__(self, ctx: rt.Context, plan: SwapPlan, codec: str | dict = "ce"):
+    def __init__(self, ctx: rt.Context, plan: SwapPlan, codec: str | dict = "ce", zx_max_ratio: float | None = None):
         self.ctx = ctx
         self.plan = plan
         self.codec = codec
+        self.zx_max_ratio = self.ZX_MAX_RATIO if zx_max_ratio is None else zx_max_ratio
         self.last_stats = {}
         self.handle_tensor: dict[int, int] = {}   # lms handle id -> captured graph tensor id (last step)
         # window probe (LMS.tune_windows): {"ranks": node ranks to clock} -> the run
@@ -764,10 +765,29 @@ class SwapExecutor:
     # a sign bit instead of 8 bits).  ResNet-50 at 908: ZX on both kinds
     # 331 img/s, ZX on ReLU outputs only 321 (profiles/r02/README.md).
     ZX_MAX_RATIO = 0.92
+    # ... but an encoded transfer is moved by SM kernels that stay resident for
+    # the whole (link-bound) copy, next to the compute stream's kernels.  When
+    # the step's swap traffic is short next to its compute, the link has time
+    # to spare and those SM slots only slow the compute down: ResNet-50 at
+    # 1.25x B0 (4.9 GB swapped): copy engine 754.8 img/s, ZX on ReLU outputs
+    # 736.7, ZX on everything 623.1; at 4.7x B0 (55 GB): ZX on everything is
+    # the fastest (profiles/r02/README.md).
+    @staticmethod
+    def zx_policy(link_s: float, compute_s: float) -> float:
+        """ZX threshold for a step whose swaps take ``link_s`` on the copy engine and
+        whose compute takes ``compute_s``: none while the link is not the bottleneck,
+        only clearly compressible tensors (ReLU outputs) near balance, every tensor
+        the codec shrinks once the link decides the step."""
+        r = link_s / max(compute_s, 1e-9)
+        if r < 0.6:
+            return 0.0
+        if r < 1.2:
+            return 0.6
+        return 0.92
 
     def _codec_for(self, si: int, t) -> str:
         if self.codec == "auto":
-            return "zx" if self.plan.saved[si].zx_ratio <= self.ZX_MAX_RATIO else "ce"
+            return "zx" if self.plan.saved[si].zx_ratio <= self.zx_max_ratio else "ce"
         if isinstance(self.codec, str):
             return self.codec
         return self.codec.get(si, "ce")
@@ -956,8 +976,23 @@ class LMS:
         self._drop_step_plan()
         self.cfg = cfg
         self.plan = build_plan(self.graph, self.meta, cfg, 0, self.far_cfg, self.far_max_fraction)
-        self._exec = SwapExecutor(self.ctx, self.plan, self.codec)
+        self._exec = SwapExecutor(self.ctx, self.plan, self.codec, self._zx_threshold(self.plan))
         return self.plan
+
+    link_context = None   # (copy-engine GB/s, compute s per step, capture bytes -> step bytes)
+
+    def set_link_context(self, link_gbs: float, compute_s: float, bytes_scale: float):
+        """Let ``codec="auto"`` weigh each plan's swap traffic against the step's
+        compute (``SwapExecutor.zx_policy``)."""
+        self.link_context = (link_gbs, compute_s, bytes_scale)
+        if self.plan is not None:
+            self._exec.zx_max_ratio = self._zx_threshold(self.plan)
+
+    def _zx_threshold(self, plan) -> float:
+        if self.link_context is None:
+            return SwapExecutor.ZX_MAX_RATIO
+        gbs, compute_s, scale = self.link_context
+        return SwapExecutor.zx_policy(plan.swapped_bytes_per_step * scale / (gbs * 1e9), compute_s)
 
     PLAN_ATTEMPTS = 3
     # replay steps that re-place the plan with the lifetimes they observe (the
@@ -1164,11 +1199,12 @@ class LMS:
                 if s.tid in self.meta["saved_tensor_id"]}
         return LinkModel(d2h_ce=link_gbs["d2h"] * 1e9, h2d_ce=link_gbs["h2d"] * 1e9,
                          d2h_zc=zc_efficiency * link_gbs["d2h"] * 1e9, h2d_zc=zc_efficiency * link_gbs["h2d"] * 1e9,
-                         wire_ratio=wire, zx_max_ratio=SwapExecutor.ZX_MAX_RATIO)
+                         wire_ratio=wire, zx_max_ratio=self._exec.zx_max_ratio if self._exec else
+                         SwapExecutor.ZX_MAX_RATIO)
 
     def _set_plan(self, plan: SwapPlan):
         self.plan = plan
-        self._exec = SwapExecutor(self.ctx, plan, self.codec)
+        self._exec = SwapExecutor(self.ctx, plan, self.codec, self._zx_threshold(plan))
         self._drop_step_plan()
 
     def _timed_replay(self, x, y, steps: int = 5, agree=None):
