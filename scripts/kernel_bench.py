@@ -123,7 +123,7 @@ def main():
                                            "ms": t * 1e3}
 
     # host-link transfers through the swap engine (per-transfer CUDA events on the copy streams)
-    def swap_rates(codec, t_in):
+    def swap_rates(codec, t_in, settled=False):
         ctx.synchronize()
         ctx.trace_clear()
         hs = []
@@ -131,6 +131,9 @@ def main():
         dst = torch.empty_like(t_in)
         for _ in range(max(2, args.iters)):
             h = ctx.swap_out(t_in, codec, s)
+            if settled:   # the swap-out landed before the swap-in is issued, as in a training step
+                torch.cuda.synchronize()
+                ctx.synchronize()
             ctx.swap_in(h, dst, trigger_stream=s)
             ctx.wait(h, s)
             hs.append(h)
@@ -163,6 +166,9 @@ def main():
         res["swap_zvc_dense"] = swap_rates("zvc", dense)
         res["swap_zx_relu"] = swap_rates("zx", relu)
         res["swap_zx_dense"] = swap_rates("zx", dense)
+        # swap-ins issued after their swap-out landed (as in a training step)
+        res["swap_zx_dense_settled"] = swap_rates("zx", dense, settled=True)
+        res["swap_zx_relu_settled"] = swap_rates("zx", relu, settled=True)
         res["swap_ce_relu"] = swap_rates("ce", relu)
         # strided views (not dense in memory): channels-last view of NCHW and a channel slice
         xv = torch.randn(max(1, n // (64 * 56 * 56)), 64, 56, 56, device=dev)

@@ -148,10 +148,15 @@ def test_zx_exponent_planes_roundtrip(lms_ctx, n):
 
 
 def test_zx_swap_roundtrip_and_wire(lms_ctx):
+    """ZX round trips of a dense and a ReLU tensor issued after the swap-out landed."""
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(64, 256, 28, 28, device="cuda", generator=g)
+    lms_ctx.synchronize()
+    lms_ctx.trace_clear()
     for codec in ("zx", "zvc"):
         h = lms_ctx.swap_out(x, codec)
+        torch.cuda.synchronize()
+        lms_ctx.synchronize()      # the stream's tile table is readable: the exact wire size is known
         out = lms_ctx.swap_in(h)
         lms_ctx.wait(h)
         torch.cuda.synchronize()
@@ -163,3 +168,12 @@ def test_zx_swap_roundtrip_and_wire(lms_ctx):
             assert wire < 0.92 * x.numel() * 4
         else:
             assert wire >= x.numel() * 4   # dense: ZVC keeps raw tiles
+    r = torch.relu(x)
+    h = lms_ctx.swap_out(r, "zx")
+    torch.cuda.synchronize()
+    lms_ctx.synchronize()
+    out = lms_ctx.swap_in(h)
+    lms_ctx.wait(h)
+    torch.cuda.synchronize()
+    assert torch.equal(out, r)
+    lms_ctx.release(h)
