@@ -268,6 +268,7 @@ struct lms_ctx {
   uint64_t trace_gen = 0;   // bumped by lms_trace_clear
   int use_bulk = 1;         // ZVC kernels move chunks with cp.async.bulk (LMS_ZVC_BULK=0: STG/LDG)
   int zc_ctas = 0;          // CTAs of the zero-copy (host-side) kernels
+  int zc_dec_ctas = 0;      // ... of the zero-copy decode (0: zc_ctas; LMS_ZC_DEC_CTAS)
   int use_tma_pack = 1;     // pack/unpack of rows layouts through tensor maps (LMS_TMA_PACK=0: SIMT)
   // strided (non-dense) swaps: packed/unpacked in HBM by the TMA kernels through a
   // staging block owned by each copy channel, moved by the copy engine
@@ -1242,7 +1243,8 @@ int launch_zvc_encode(lms_ctx* c, const uint32_t* src, uint64_t nwords, char* ou
 int launch_zvc_decode(lms_ctx* c, const char* enc, uint64_t nwords, uint32_t* dst, cudaStream_t s,
                       bool from_host) {
   int grid = sm_grid(c, int64_t(zvc_tiles(nwords)), 1);
-  if (from_host) grid = int(std::min<int64_t>(int64_t(zvc_tiles(nwords)), c->zc_ctas));
+  if (from_host)
+    grid = int(std::min<int64_t>(int64_t(zvc_tiles(nwords)), c->zc_dec_ctas > 0 ? c->zc_dec_ctas : c->zc_ctas));
   zvc_decode_kernel<<<std::max(grid, 1), 256, kZvcSmemBytes, s>>>(enc, nwords, dst, c->use_bulk);
   c->st.kernel_launches++;
   CK(cudaGetLastError());
@@ -1332,6 +1334,7 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
   // in flight on the link), overridable for tuning
   c->zc_ctas = cfg->sm_ctas > 0 ? cfg->sm_ctas : c->num_sms;
   if (const char* v = getenv("LMS_ZC_CTAS")) c->zc_ctas = std::max(1, atoi(v));
+  if (const char* v = getenv("LMS_ZC_DEC_CTAS")) c->zc_dec_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("LMS_ZVC_BULK")) c->use_bulk = atoi(v) != 0;
   if (const char* v = getenv("LMS_TMA_PACK")) c->use_tma_pack = atoi(v) != 0;
   if (const char* v = getenv("LMS_STAGE_STRIDED")) c->stage_strided = atoi(v) != 0;
