@@ -268,7 +268,7 @@ struct lms_ctx {
   uint64_t trace_gen = 0;   // bumped by lms_trace_clear
   int use_bulk = 1;         // ZVC kernels move chunks with cp.async.bulk (LMS_ZVC_BULK=0: STG/LDG)
   int zc_ctas = 0;          // CTAs of the zero-copy (host-side) kernels
-  int zc_dec_ctas = 0;      // ... of the zero-copy decode (0: zc_ctas; LMS_ZC_DEC_CTAS)
+  int zc_dec_ctas = 0;      // ... of the zero-copy decode (LMS_ZC_DEC_CTAS)
   int use_tma_pack = 1;     // pack/unpack of rows layouts through tensor maps (LMS_TMA_PACK=0: SIMT)
   // strided (non-dense) swaps: packed/unpacked in HBM by the TMA kernels through a
   // staging block owned by each copy channel, moved by the copy engine
@@ -1334,6 +1334,11 @@ int lms_create(const lms_config_t* cfg, lms_ctx** out) {
   // in flight on the link), overridable for tuning
   c->zc_ctas = cfg->sm_ctas > 0 ? cfg->sm_ctas : c->num_sms;
   if (const char* v = getenv("LMS_ZC_CTAS")) c->zc_ctas = std::max(1, atoi(v));
+  // decode CTAs (LMS_ZC_DEC_CTAS): 37 / 56 / 74 / 100 / 148 all keep the H2D
+  // wire rate; at 908 the step measured 334.5 / 335.3 / 354.5 / 338.2 / 337.3
+  // img/s, within the run-to-run spread of the swapped bytes (52.0 - 54.5 GB
+  // per direction), so the decode keeps the encode's count
+  c->zc_dec_ctas = c->zc_ctas;
   if (const char* v = getenv("LMS_ZC_DEC_CTAS")) c->zc_dec_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("LMS_ZVC_BULK")) c->use_bulk = atoi(v) != 0;
   if (const char* v = getenv("LMS_TMA_PACK")) c->use_tma_pack = atoi(v) != 0;
@@ -1446,7 +1451,7 @@ int lms_reset_peaks(lms_ctx* c) {
 int lms_set_tuning(lms_ctx* c, int zc_ctas, int use_bulk, int use_tma_pack) {
   if (!c) return fail(LMS_E_INVALID, "null ctx");
   std::lock_guard<std::mutex> g(c->mu);
-  if (zc_ctas > 0) c->zc_ctas = zc_ctas;
+  if (zc_ctas > 0) c->zc_ctas = c->zc_dec_ctas = zc_ctas;
   if (use_bulk >= 0) c->use_bulk = use_bulk != 0;
   if (use_tma_pack >= 0) c->use_tma_pack = use_tma_pack != 0;
   return LMS_OK;
