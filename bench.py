@@ -22,6 +22,7 @@ identities) and prints the same metric.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import gc
 import json
 import math
@@ -87,6 +88,9 @@ def parse():
                     help="wall-clock budget of the joint search (candidates started after it are skipped)")
     ap.add_argument("--ddp", action="store_true",
                     help="wrap the model in DistributedDataParallel even at one rank (exercises the DP path)")
+    ap.add_argument("--backend", default=os.environ.get("LMS_BENCH_BACKEND", "nccl"), choices=("nccl", "gloo"),
+                    help="process-group backend for N>1; gloo lets N ranks share fewer GPUs "
+                         "(rank r on GPU r %% device_count) to exercise the multi-rank path on a one-GPU box")
     ap.add_argument("--quick", action="store_true", help="small budget for a fast smoke of the bench")
     return ap.parse_args()
 
@@ -218,7 +222,9 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a GPU (no CPU fallback)")
-    dev = torch.device("cuda", local)
+    # one rank per GPU; with --backend gloo, ranks may share a GPU (local % device_count)
+    gpu = local % torch.cuda.device_count() if args.backend == "gloo" else local
+    dev = torch.device("cuda", gpu)
     budget = int(args.budget_gib * GIB) if not args.quick else 4 * GIB
 
     # the pool must own PyTorch's allocator before anything lazily initialises CUDA
@@ -227,9 +233,9 @@ def main():
     # enforced by the host pool so the box never pages or OOM-kills
     local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", ws))
     host_cap = max(1 * GIB, int(0.6 * host_available() / max(1, local_ws)) - 4 * GIB)
-    ctx = rt.Context(device=local, device_reserve=budget, host_chunk=4 * GIB, timing=True, host_limit=host_cap)
+    ctx = rt.Context(device=gpu, device_reserve=budget, host_chunk=4 * GIB, timing=True, host_limit=host_cap)
     rt.install_allocator(ctx)
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(gpu)
     # the link's copy-engine peak, measured first while the pool is empty
     link = measure_host_link(torch, dev)
     gc.collect()
@@ -238,7 +244,10 @@ def main():
         import torch.distributed as dist
         for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511"), ("RANK", "0"), ("WORLD_SIZE", "1")):
             os.environ.setdefault(k, v)
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     torch.backends.cudnn.benchmark = False          # autotuning would probe workspaces past the budget
     torch.backends.cudnn.allow_tf32 = bool(args.tf32)
@@ -255,7 +264,7 @@ def main():
         shape_desc = f"{args.arch} {size}^2 fp32"
     base_model = model
     if use_dist:
-        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[gpu])
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
     loss_fn = torch.nn.functional.cross_entropy
 
@@ -277,8 +286,9 @@ def main():
     def fits(n) -> bool:
         try:
             x, y = batch(n)
-            for _ in range(2):
-                plain_step(x, y)
+            with local_probe():
+                for _ in range(2):
+                    plain_step(x, y)
             torch.cuda.synchronize(dev)
             ok = True
         except RuntimeError as e:
@@ -303,9 +313,30 @@ def main():
             return
         model = None
         gc.collect()
-        model = torch.nn.parallel.DistributedDataParallel(base_model, device_ids=[local])
+        model = torch.nn.parallel.DistributedDataParallel(base_model, device_ids=[gpu])
         if lms is not None:
             lms.model = model
+
+    @contextlib.contextmanager
+    def local_probe():
+        """Fit probes run the unwrapped model: a probe may OOM on one rank only
+        (frees wait on each rank's own transfers), and a rank failing mid-step
+        must not leave a peer inside a DDP collective.  ``agree`` combines the
+        verdicts afterwards; the parameters' memory is the same either way."""
+        nonlocal model
+        if not use_dist:
+            yield
+            return
+        wrapped = model
+        model = base_model
+        if lms is not None:
+            lms.model = base_model
+        try:
+            yield
+        finally:
+            model = wrapped
+            if lms is not None:
+                lms.model = wrapped
 
     def tune_agree(v, op):
         """The tuner's decisions common to every DDP rank (None without DDP)."""
@@ -484,8 +515,9 @@ def main():
         lms.static_plan = False   # fit probes run on the dynamic pool; the timed run plans
         xb, yb = batch(nb, seed=7)
         try:
-            for _ in range(2):
-                lms.step(xb, yb)
+            with local_probe():
+                for _ in range(2):
+                    lms.step(xb, yb)
             torch.cuda.synchronize(dev)
             ok = True
         except RuntimeError as e:
@@ -580,7 +612,7 @@ def main():
                                  ctrld_strategy=args.strategy, swap_branches=args.branches,
                                  branch_threshold=args.branch_threshold, fuse_swapins=args.fuse_swapins,
                                  swapin_fuse_distance=args.fuse_distance))
-        clocks = Clocks(local)
+        clocks = Clocks(gpu)
         tuned = {}
         try:
             if tune and prepared is not None:
@@ -828,7 +860,7 @@ def main():
                    "budget_gib": budget / GIB, "no_swap_max_batch": b0,
                    "batch_ratio": round(bs / b0, 3) if b0 else None, "input_size": size,
                    "host_limit_gib_per_rank": round(host_cap / GIB, 1), "host_limited": host_limited,
-                   "parallelism": f"dp{ws}" if use_dist else "single",
+                   "parallelism": f"dp{ws}" if use_dist else "single", "pg_backend": args.backend if use_dist else None,
                    "l2": "inputs (>=450 MB/step) exceed L2; no flush",
                    "rewrite": {"lb": args.lb, "ub": args.ub, "ctrld_strategy": args.strategy,
                                "fuse_swapins": args.fuse_swapins, "n_tensors": plan.report.tensors_swapped,
