@@ -49,3 +49,32 @@ def test_swapped_ddp_matches_plain_ddp(tmp_path):
         if v.is_floating_point() and "running" not in k:
             assert torch.equal(swap[1]["state"][k], v), k
     assert swap[0]["facts"]["tuned"].get("steps_per_trial") == swap[1]["facts"]["tuned"].get("steps_per_trial")
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_bench_two_ranks_one_json_line():
+    """bench.py's N>1 contract under torchrun: ranks agree on every fit/tuning
+    decision, time with a barrier and take the max over ranks, and rank 0
+    alone prints ONE JSON line whose value counts both ranks' images.  (gloo
+    lets both ranks share the box's one GPU; --quick keeps it to ~1.5 min.)"""
+    import json
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--quick", "--backend", "gloo", "--cpu-baseline", "0"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2" and d["config"]["pg_backend"] == "gloo"
+    bs = d["config"]["per_gpu_batch"]
+    assert d["config"]["global_batch"] == 2 * bs
+    # whole-job throughput from the max-over-ranks step time
+    assert abs(d["value"] - 2 * bs * 1000.0 / d["ms_per_step"]) < 0.01 * d["value"]
+    assert d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
