@@ -244,10 +244,14 @@ def main():
         import torch.distributed as dist
         for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511"), ("RANK", "0"), ("WORLD_SIZE", "1")):
             os.environ.setdefault(k, v)
+        # a rank stranded in a collective (a peer died mid-step) errors out
+        # instead of holding the job until the default 10-30 min watchdog
+        from datetime import timedelta
+        pg_timeout = timedelta(seconds=float(os.environ.get("LMS_BENCH_PG_TIMEOUT_S", "900")))
         if args.backend == "gloo":
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=pg_timeout)
         else:
-            dist.init_process_group("nccl", device_id=dev)
+            dist.init_process_group("nccl", device_id=dev, timeout=pg_timeout)
 
     torch.backends.cudnn.benchmark = False          # autotuning would probe workspaces past the budget
     torch.backends.cudnn.allow_tf32 = bool(args.tf32)
@@ -620,7 +624,7 @@ def main():
                 lms._set_plan(prepared[1])
                 # record the chosen plan once more and time it: the timed run then
                 # replays exactly this recorded placement
-                final = lms._timed_replay(xs, ys, 5, tune_agree)
+                final = lms.time_replay(xs, ys, 5, tune_agree)
                 tuned = dict(prepared[2], reused=True, final_ms=final["ms"] if final else None,
                              final_spread_ms=final["spread"] if final else None)
                 prepared = None     # a retry (OOM) tunes afresh

@@ -238,6 +238,7 @@ struct lms_ctx {
     int64_t rclock = 0;
     uint64_t refinements = 0;
     size_t cursor = 0;
+    size_t resyncs = 0;   // this replay's allocations off the recorded sequence
     bool diverged = false;
     std::map<size_t, std::pair<size_t, size_t>> live;  // off -> (size, item)
     std::vector<PlanFreed> freed;
@@ -437,6 +438,9 @@ void drain_holds(lms_ctx* c, char* base) {
   }
 }
 
+constexpr size_t kPlanMaxResyncs = 32;
+constexpr size_t kPlanSkipAhead = 8;   // recorded allocations a replay may skip in a row
+
 // replay: serve the next recorded allocation from its planned offset.
 // Returns 1 when this request is not planned (the dynamic pool serves it).
 int plan_alloc(lms_ctx* c, size_t rsize, void* stream, void** out) {
@@ -445,13 +449,31 @@ int plan_alloc(lms_ctx* c, size_t rsize, void* stream, void** out) {
     P.diverged = true;
     return 1;
   }
-  const size_t idx = P.cursor++;
-  const PlanItem& it = P.items[idx];
-  if (it.size != rsize) {
-    P.diverged = true;  // the step allocates differently from the recorded one
-    P.diverged_steps++;
-    return 1;
+  size_t idx = P.cursor++;
+  if (P.items[idx].size != rsize) {
+    // an allocation the recording did not make (a DDP buffer broadcast's
+    // staging tensor, say) is served by the dynamic pool and the cursor stays;
+    // recorded allocations this step did not make (up to kPlanSkipAhead in a
+    // row) are stepped over when a following item matches.  Past
+    // kPlanMaxResyncs per step the sequences differ.
+    if (P.resyncs >= kPlanMaxResyncs) {
+      P.diverged = true;  // the step allocates differently from the recorded one
+      P.diverged_steps++;
+      return 1;
+    }
+    P.resyncs++;
+    size_t j = idx + 1;
+    const size_t end = std::min(P.items.size(), idx + 1 + kPlanSkipAhead);
+    while (j < end && P.items[j].size != rsize) ++j;
+    if (j < end) {
+      idx = j;              // items idx..j-1 were not requested this step
+      P.cursor = j + 1;
+    } else {
+      P.cursor = idx;       // an extra allocation: retry item idx on the next request
+      return 1;
+    }
   }
+  const PlanItem& it = P.items[idx];
   if (!it.planned) return 1;
   const size_t lo = it.off, hi = it.off + it.size;
   // a planned block still live over this range means the sequences drifted
@@ -1508,6 +1530,7 @@ int lms_plan_begin(lms_ctx* c, int mode) {
   } else if (mode == LMS_PLAN_REPLAY || mode == LMS_PLAN_REFINE) {
     if (!P.ready) return fail(LMS_E_STATE, "no recorded plan");
     P.cursor = 0;
+    P.resyncs = 0;
     P.diverged = false;
     if (mode == LMS_PLAN_REFINE) {
       P.refine = P.items;
@@ -1529,7 +1552,7 @@ int lms_plan_end(lms_ctx* c) {
   if (mode == LMS_PLAN_REFINE) {
     // re-place with the lifetimes this replay step showed; adopt the new
     // placement only if it fits the region already held
-    if (P.diverged || !P.live.empty()) return LMS_OK;
+    if (P.diverged || P.resyncs || !P.live.empty()) return LMS_OK;
     std::vector<PlanItem> nx = P.refine;
     for (size_t i = 0; i < nx.size(); ++i) {
       if (!P.items[i].planned) {

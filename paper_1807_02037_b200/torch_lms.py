@@ -32,6 +32,7 @@ cannot be hooked on its forward execution).
 
 from __future__ import annotations
 
+import contextlib
 import time
 from dataclasses import dataclass, field
 
@@ -926,6 +927,34 @@ class SwapExecutor:
         return loss
 
 
+def _snapshot_training_state(module: torch.nn.Module, optimizer) -> dict:
+    """Host copies of a module's parameters and buffers and of its optimizer's
+    per-parameter state (restored by ``_restore_training_state``)."""
+    with torch.no_grad():
+        return {"module": [t.detach().to("cpu", copy=True) for t in (*module.parameters(), *module.buffers())],
+                "opt": {p: {k: ((v.detach().to("cpu", copy=True), v.device) if torch.is_tensor(v) else (v, None))
+                            for k, v in st.items()}
+                        for p, st in optimizer.state.items()}}
+
+
+def _restore_training_state(module: torch.nn.Module, optimizer, saved: dict) -> None:
+    with torch.no_grad():
+        for t, v in zip((*module.parameters(), *module.buffers()), saved["module"]):
+            t.copy_(v)
+        for p in list(optimizer.state):
+            if p not in saved["opt"]:
+                del optimizer.state[p]
+        for p, st in saved["opt"].items():
+            cur = optimizer.state[p]
+            for k, (v, dev) in st.items():
+                c = cur.get(k)
+                if dev is not None and torch.is_tensor(c) and c.shape == v.shape and c.device == dev:
+                    c.copy_(v)
+                else:
+                    cur[k] = v.to(dev) if dev is not None else v
+    optimizer.zero_grad(set_to_none=True)
+
+
 class LMS:
     """TFLMS for a PyTorch training step: capture once, rewrite, then train with swapping.
 
@@ -1059,7 +1088,46 @@ class LMS:
         very placement that was timed.  Under DDP every rank must take the same
         number of steps: ``agree(value, op)`` (an all-reduce, op "max"/"min")
         makes every timing- and memory-dependent decision common to all ranks
-        (slowest rank's times, any rank's failure)."""
+        (slowest rank's times, any rank's failure).
+
+        Under DDP (``agree`` given and the model a ``DistributedDataParallel``)
+        tuning is side-effect free and collective-free inside a step: trials run
+        the wrapped module's local replica (no gradient all-reduce), so a rank
+        that hits the budget mid-step strands no peer in a collective; it keeps
+        joining every ``agree`` with a failure vote instead.  The weights,
+        buffers and optimizer state are restored at the end, so the replicas
+        stay identical."""
+        with self._local_replica(agree):
+            return self._tune_windows(x, y, lbs, margin, require_faster, steps, agree)
+
+    @contextlib.contextmanager
+    def _local_replica(self, agree):
+        """Under DDP with ``agree``: run the wrapped module alone (no collective
+        inside a step) and put weights, buffers and optimizer state back after.
+        The step plan recorded on the local replica is dropped on the way out:
+        the wrapped steps allocate more (buffer broadcasts, bucket rebuilds), so
+        they record their own (the swap plan and its tuned windows stay)."""
+        ddp = self.model if isinstance(self.model, torch.nn.parallel.DistributedDataParallel) else None
+        if agree is None or ddp is None:
+            yield
+            return
+        saved = _snapshot_training_state(ddp.module, self.optimizer)
+        self.model = ddp.module
+        try:
+            yield
+        finally:
+            self.model = ddp
+            _restore_training_state(ddp.module, self.optimizer, saved)
+            self._drop_step_plan()
+
+    def time_replay(self, x, y, steps: int = 5, agree=None):
+        """Record the current plan once more and time ``steps`` replayed steps
+        (``_timed_replay``); under DDP on the local replica like ``tune_windows``.
+        The next steps replay the placement that was timed."""
+        with self._local_replica(agree):
+            return self._timed_replay(x, y, steps, agree)
+
+    def _tune_windows(self, x, y, lbs, margin, require_faster, steps, agree) -> dict:
         from dataclasses import replace
         import numpy as np
         if not self.static_plan or self.plan is None:
@@ -1081,15 +1149,23 @@ class LMS:
             return v if agree is None else agree(v, op)
 
         self._drop_step_plan()
-        while self._plan_step != 1:
-            self.step(x, y)
-        self._exec.probe = probe = {"ranks": ranks}
+        probe = {"ranks": ranks}
+        ok = True
         try:
-            self.step(x, y)
-        finally:
-            self._exec.probe = None
-        torch.cuda.synchronize()
-        if common(1.0 if self.plan_note == "region" else 0.0, "min") < 0.5:
+            while self._plan_step != 1:
+                self.step(x, y)
+            self._exec.probe = probe
+            try:
+                self.step(x, y)
+            finally:
+                self._exec.probe = None
+            torch.cuda.synchronize()
+        except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
+            if agree is None:
+                raise
+            ok = False      # vote failure below; no collective was left half-done
+            self._after_oom()
+        if common(1.0 if ok and self.plan_note == "region" else 0.0, "min") < 0.5:
             self._drop_step_plan()
             return {}
         info = self.ctx.plan_info()
@@ -1214,34 +1290,45 @@ class LMS:
         lifetimes or a step hits the budget.  The step count is fixed, so DDP ranks
         stay in step; ``agree`` makes the outcome common (slowest rank, any failure)."""
         self._drop_step_plan()
+        failed = False
+
+        def run_step():
+            # under ``agree`` a rank that hits the budget stops stepping but keeps
+            # voting, so every rank makes the same sequence of all-reduces
+            nonlocal failed
+            if failed:
+                return
+            try:
+                self.step(x, y)
+            except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
+                if agree is None:
+                    raise
+                failed = True
+                self._after_oom()
+
         per = None
         try:
             # dynamic step, recorded step, first replay; a recording whose placement
             # did not fit is retried (at most 6 setup steps; under DDP the ranks
             # agree on when every one of them is done)
             for _ in range(6):
-                done = self._plan_step >= 3 or self.plan_note == "no-fit"
+                done = failed or self._plan_step >= 3 or self.plan_note == "no-fit"
                 if agree is not None:
                     done = agree(1.0 if done else 0.0, "min") > 0.5
                 if done:
                     break
-                self.step(x, y)
-            fits = self.plan_note == "region" and self.ctx.plan_info()["alpha"] >= 1.0
+                run_step()
+            fits = not failed and self.plan_note == "region" and self.ctx.plan_info()["alpha"] >= 1.0
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
             torch.cuda.synchronize()
             evs[0].record()
             for k in range(steps):
-                self.step(x, y)
+                run_step()
                 evs[k + 1].record()
             torch.cuda.synchronize()
-            per = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(steps)) if fits else None
+            per = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(steps)) if fits and not failed else None
         except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
-            if agree is not None:
-                raise     # a rank that failed mid-step cannot rejoin its peers' collectives
-            self.optimizer.zero_grad(set_to_none=True)
-            torch.cuda.synchronize()
-            self.ctx.synchronize()
-            self._drop_step_plan()
+            self._after_oom()       # agree is None here: run_step re-raised
         if agree is not None:
             if agree(0.0 if per is None else 1.0, "min") < 0.5:
                 return None
@@ -1266,6 +1353,14 @@ class LMS:
             ev.append(TraceEvent(r["end_ms"] * 1e-3, "xfer_finish", None, tid, r["wire_bytes"], where))
         ev.sort(key=lambda e: e.time)
         return ev
+
+    def _after_oom(self):
+        """Clean up after a step that hit the budget: no gradients, idle streams,
+        no half-recorded plan."""
+        self.optimizer.zero_grad(set_to_none=True)
+        torch.cuda.synchronize()
+        self.ctx.synchronize()
+        self._drop_step_plan()
 
     def _drop_step_plan(self):
         if self._plan_step >= 2 or self.plan_note == "region":

@@ -71,8 +71,8 @@ def main():
                   codec="auto")
         lms.capture(*batch(99, 4))
         facts["tuned"] = lms.tune_windows(*batches[0], steps=2, agree=agree)
-        base.load_state_dict(init)     # the tuner's trial steps moved the (replicated) weights
-        opt.state.clear()
+        # under DDP the tuner runs the local replica and restores the training state
+        facts["tune_restored"] = all(torch.equal(v, init[k]) for k, v in base.state_dict().items())
         ctx.trace_clear()
         losses = [lms.step(x, y).detach().clone() for x, y in batches]
         torch.cuda.synchronize()

@@ -23,7 +23,7 @@ GIB = 1 << 30
 
 
 def _launch(tmp_path, mode, budget):
-    env = dict(os.environ, LMS_TEST_NO_POOL="1", CUDNN_CONV_WSCAP_DBG="128", LMS_PAGE_MB="16")
+    env = dict(os.environ, LMS_TEST_NO_POOL="1", CUDNN_CONV_WSCAP_DBG="128", LMS_PAGE_MB="8")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29533", WORKER, mode, str(tmp_path), f"{budget:.3f}"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
@@ -36,11 +36,12 @@ def test_swapped_ddp_matches_plain_ddp(tmp_path):
     import torch
     plain = _launch(tmp_path, "plain", 8.0)
     peak = max(p["facts"]["peak"] for p in plain)
-    budget = 0.85 * peak / GIB
+    budget = 0.9 * peak / GIB
     swap = _launch(tmp_path, "swap", budget)
     for r in range(2):
         f = swap[r]["facts"]
         assert f["d2h"] > 0 and f["swapped"] > 10
+        assert f["tune_restored"]
         assert f["peak"] <= budget * GIB < peak
         for k, v in plain[r]["state"].items():
             assert torch.equal(swap[r]["state"][k], v), (r, k)
@@ -67,7 +68,8 @@ def test_bench_two_ranks_one_json_line():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--quick", "--backend", "gloo", "--cpu-baseline", "0"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    env = dict(os.environ, LMS_BENCH_PG_TIMEOUT_S="180")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
     assert len(lines) == 1, r.stdout[-3000:]

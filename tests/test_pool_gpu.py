@@ -148,3 +148,51 @@ def test_plan_record_replay_refine_keeps_data(lms_ctx):
     finally:
         torch.cuda.synchronize()
         ctx.close()
+
+
+def test_plan_replay_tolerates_extra_and_skipped_allocations(lms_ctx):
+    """A replayed step that makes one allocation the recording did not (e.g. DDP's
+    buffer-broadcast staging tensor) and skips two it did: the extra one is served
+    by the dynamic pool, the skipped ones are stepped over, the rest still replay
+    from their planned offsets (no divergence), and every block keeps its bytes."""
+    ctx = rt.Context(device=0, device_reserve=512 * MIB, timing=False)
+    sizes = [8 * MIB, 24 * MIB, 3 * MIB, 40 * MIB, 8 * MIB, 1 * MIB, 16 * MIB]
+
+    def run(step, extra_at=None, skip=()):
+        blocks = []
+        for i, n in enumerate(sizes):
+            if i == extra_at:
+                e = ctx.dev_alloc(64 * 1024)
+                _view(e, 64 * 1024).fill_(99)
+                blocks.append((e, 64 * 1024, 99))
+            if i in skip:
+                continue
+            p = ctx.dev_alloc(n)
+            _view(p, n).fill_((i * 13 + step) % 251)
+            blocks.append((p, n, (i * 13 + step) % 251))
+        for p, n, v in blocks:
+            assert bool((_view(p, n) == v).all()), (step, p)
+        for p, _, _ in reversed(blocks):
+            ctx.dev_free(p)
+        torch.cuda.synchronize()
+
+    try:
+        run(0)
+        ctx.plan_begin(rt.PLAN_RECORD)
+        run(1)
+        ctx.plan_end()
+        ctx.plan_begin(rt.PLAN_REPLAY)
+        run(2)
+        ctx.plan_end()
+        base = ctx.plan_info()
+        ctx.plan_begin(rt.PLAN_REPLAY)
+        run(3, extra_at=2, skip=(4, 5))
+        ctx.plan_end()
+        info = ctx.plan_info()
+        assert info["diverged_steps"] == base["diverged_steps"] == 0
+        assert info["hits"] - base["hits"] == len(sizes) - 2       # all but the skipped ones planned
+        assert info["dynamic"] - base["dynamic"] == 1              # the extra one
+        ctx.plan_reset()
+    finally:
+        torch.cuda.synchronize()
+        ctx.close()
