@@ -226,6 +226,8 @@ def main():
     gpu = local % torch.cuda.device_count() if args.backend == "gloo" else local
     dev = torch.device("cuda", gpu)
     budget = int(args.budget_gib * GIB) if not args.quick else 4 * GIB
+    if args.quick:
+        os.environ.setdefault("LMS_PAGE_MB", "16")   # 256 pages in the small budget, as 64 MiB pages give 16 GiB
 
     # the pool must own PyTorch's allocator before anything lazily initialises CUDA
     # pinned host memory is shared by the ranks of this box: each gets its share

@@ -456,6 +456,10 @@ int plan_alloc(lms_ctx* c, size_t rsize, void* stream, void** out) {
     // recorded allocations this step did not make (up to kPlanSkipAhead in a
     // row) are stepped over when a following item matches.  Past
     // kPlanMaxResyncs per step the sequences differ.
+    static const bool dbg = getenv("LMS_PLAN_DEBUG") != nullptr;
+    if (dbg)
+      fprintf(stderr, "[lms plan] item %zu: recorded %llu B, requested %zu B (resync %zu)\n", idx,
+              (unsigned long long)P.items[idx].size, rsize, P.resyncs);
     if (P.resyncs >= kPlanMaxResyncs) {
       P.diverged = true;  // the step allocates differently from the recorded one
       P.diverged_steps++;

@@ -1079,7 +1079,8 @@ class LMS:
         of those moves whose placement the pool's solver fits is then tried
         for real: re-targeted (``retarget``), re-recorded and one replayed step
         timed against the untouched plan; the set shrinks by a third until a replay
-        fits and is faster, or dropped.  The model parameters move by the
+        fits and is faster, or dropped (when the untouched plan's own recording
+        does not fit, the full set gets one try).  The model parameters move by the
         probe and trial steps (like ``autotune``).  Returns a summary dict;
         ``{}`` changes nothing (no room, or no static plan to measure).
 
@@ -1105,8 +1106,10 @@ class LMS:
         """Under DDP with ``agree``: run the wrapped module alone (no collective
         inside a step) and put weights, buffers and optimizer state back after.
         The step plan recorded on the local replica is dropped on the way out:
-        the wrapped steps allocate more (buffer broadcasts, bucket rebuilds), so
-        they record their own (the swap plan and its tuned windows stay)."""
+        the wrapped steps allocate differently (a bucket rebuild on a fresh
+        wrapper's second step takes ~the gradients' bytes before the old
+        buckets go), so they record their own; the swap plan and its tuned
+        windows stay."""
         ddp = self.model if isinstance(self.model, torch.nn.parallel.DistributedDataParallel) else None
         if agree is None or ddp is None:
             yield
@@ -1222,14 +1225,16 @@ class LMS:
         base_ms = base["ms"] if base else None
         trials, spreads = {}, {"base": base["spread"] if base else None}
         chosen = 0
-        while keep > 0 and base_ms is not None:
+        while keep > 0:
             self._set_plan(retarget(orig, {m[0]: m[4] for m in moved[:keep]}))
             r = self._timed_replay(x, y, steps, agree)
             trials[keep] = r["ms"] if r else None
             spreads[keep] = r["spread"] if r else None
-            if r is not None and (r["ms"] < base_ms or not require_faster):
+            if r is not None and (base_ms is None or r["ms"] < base_ms or not require_faster):
                 chosen = keep
                 break
+            if base_ms is None:
+                break       # the untouched plan's recording did not fit either: one try with every move
             keep = keep * 2 // 3
         if not chosen:
             # the untouched plan won: replay it again so its recorded placement is the one kept
