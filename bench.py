@@ -156,20 +156,23 @@ def measure_host_link(torch, dev, nbytes=512 * MIB):
     d1 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    res = {}
+    res = {"h2d": 0.0, "d2h": 0.0}
     for _ in range(2):
         d1.copy_(h1, non_blocking=True)
         h2.copy_(d2, non_blocking=True)
     torch.cuda.synchronize(dev)
-    for name, fn in (("h2d", lambda: d1.copy_(h1, non_blocking=True)),
-                     ("d2h", lambda: h2.copy_(d2, non_blocking=True))):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(4):
-            fn()
-        e1.record()
-        torch.cuda.synchronize(dev)
-        res[name] = 4 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    # the peak is the best of 3 samples per direction: a single sample can land
+    # on host-side noise (page-cache work, another process) and read 20 % low
+    for _ in range(3):
+        for name, fn in (("h2d", lambda: d1.copy_(h1, non_blocking=True)),
+                         ("d2h", lambda: h2.copy_(d2, non_blocking=True))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(4):
+                fn()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            res[name] = max(res[name], 4 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     s1.wait_event(e0)
@@ -714,7 +717,8 @@ def main():
             joint[n] = min(ms) if ms else None
             if ms:
                 joint_plan[n] = (lms.cfg, lms.plan, info)
-            log(f"[bench] joint n_tensors={n}: {joint[n]} ms ({info.get('moved')} moved)")
+            log(f"[bench] joint n_tensors={n}: {joint[n]} ms ({info.get('moved')} moved; base "
+                f"{info.get('base_ms')}, trials {info.get('trials')}, modelled {info.get('modelled')})")
             opt.zero_grad(set_to_none=True)
             gc.collect()
         fit = {n: v for n, v in joint.items() if v is not None}
@@ -831,6 +835,13 @@ def main():
     kernel_paths = [k for k in paths if not k.endswith("copy-engine")]
     dom_key = (max(kernel_paths, key=lambda k: paths[k]["ms"]) if kernel_paths
                else max(paths, key=lambda k: paths[k]["ms"]) if paths else None)
+    if link:
+        # the link once more, now that the timed runs are over: the peak is the best seen
+        lms._drop_step_plan()          # the timed runs are over: return the plan's region
+        gc.collect()
+        torch.cuda.synchronize(dev)
+        again = measure_host_link(torch, dev)
+        link = {k: round(max(link.get(k, 0.0), again.get(k, 0.0)), 2) for k in set(link) | set(again)}
     link_peak = max(link.get("d2h", 0), link.get("h2d", 0)) if link else None
     if dom_key:
         dom_peak = link.get(dom_key.split(":")[0]) if link else None
@@ -988,11 +999,18 @@ def timed(torch, dev, ws, fn, steps, tag=None):
     torch.cuda.synchronize(dev)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     e0, e1 = evs[0], evs[-1]
+    # LMS_NCU_TIMED=1 under `ncu --profile-from-start off`: the launch list covers
+    # exactly the timed swapped steps (a number printed under ncu is never a bench value)
+    prof = tag == "swapped" and os.environ.get("LMS_NCU_TIMED") == "1"
+    if prof:
+        torch.cuda.cudart().cudaProfilerStart()
     e0.record()
     for k in range(steps):
         fn()
         evs[k + 1].record()
     torch.cuda.synchronize(dev)
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     if tag:
         STEP_MS[tag] = [round(evs[k].elapsed_time(evs[k + 1]), 1) for k in range(steps)]
     if ws > 1:

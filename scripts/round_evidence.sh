@@ -11,7 +11,9 @@ tail -c 600 gpurun_out/ev_bench_ref.json
 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/ev_bench.json 2> gpurun_out/ev_bench.log
 tail -c 300 gpurun_out/ev_bench.json; grep "\[bench\]" gpurun_out/ev_bench.log | tail -4
 if [ "${EV_NCU:-1}" = "1" ]; then
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/ev_launches.csv \
-      python bench.py --steps 2 --warmup 1 --tune-windows 0 --same-batch 0 --cpu-baseline 0 > gpurun_out/ev_ncu_bench.log 2>&1
+  # only the timed swapped steps are profiled (bench.py: LMS_NCU_TIMED)
+  LMS_NCU_TIMED=1 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
+      --log-file gpurun_out/ev_launches.csv \
+      python bench.py --steps 2 --warmup 3 --tune-windows 0 --same-batch 0 --cpu-baseline 0 > gpurun_out/ev_ncu_bench.log 2>&1
   ls -la gpurun_out/ev_launches.csv
 fi
