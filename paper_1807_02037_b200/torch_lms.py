@@ -1151,71 +1151,76 @@ class LMS:
         def common(v, op):
             return v if agree is None else agree(v, op)
 
-        self._drop_step_plan()
-        probe = {"ranks": ranks}
-        ok = True
-        try:
-            while self._plan_step != 1:
-                self.step(x, y)
-            self._exec.probe = probe
-            try:
-                self.step(x, y)
-            finally:
-                self._exec.probe = None
-            torch.cuda.synchronize()
-        except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
-            if agree is None:
-                raise
-            ok = False      # vote failure below; no collective was left half-done
-            self._after_oom()
-        if common(1.0 if ok and self.plan_note == "region" else 0.0, "min") < 0.5:
+        # the recorded step the moves are modelled on varies with transfer timing:
+        # when none of the modelled moves fits its room, record once more
+        for attempt in range(2):
             self._drop_step_plan()
-            return {}
-        info = self.ctx.plan_info()
-        items = self.ctx.plan_items()
-        T = max((max(a, b, c) for _, a, b, c in items), default=0) + 2
-        live = np.zeros(T, dtype=np.float64)
-        for size, a, b, c in items:
-            if b >= 0:
-                live[a:b] += size
-        # the next recording's room: the pages not live once this plan's region
-        # is returned, less the page the pool keeps for unplanned allocations
-        limit = info["room_bytes"] * (1.0 - margin) - (64 << 20)
-        start_peak = float(live.max()) if T else 0.0
-        node_clock = probe["node_clock"]
-        issue = sorted(((c, gid, nb) for gid, (c, nb) in probe["issue"].items() if gid in cands))
-        moved = plan_window_moves(live, node_clock, issue, cands,
-                                  {g.gid: g.trigger for g in self.plan.groups}, limit)
-        # the live bytes bound the placement from below only: keep the longest
-        # prefix of the moves (in issue order) whose recorded step, with those
-        # destinations allocated at their new clocks, still places inside the
-        # room (the pool's own solver, lms_plan_solve)
-        sizes = [it[0] for it in items]
-        t0 = [it[1] for it in items]
-        t1 = [it[2] for it in items]
-        item_at = {a: i for i, a in enumerate(t0)}
-        # a move is modelled only if its destination is the allocation made at
-        # its issue clock (same bytes up to the pool's rounding)
-        moved = [m for m in moved if m[1] in item_at and 0 <= sizes[item_at[m[1]]] - m[3] < (4 << 20)]
+            probe = {"ranks": ranks}
+            ok = True
+            try:
+                while self._plan_step != 1:
+                    self.step(x, y)
+                self._exec.probe = probe
+                try:
+                    self.step(x, y)
+                finally:
+                    self._exec.probe = None
+                torch.cuda.synchronize()
+            except (torch.OutOfMemoryError, rt.LmsOutOfMemoryError):
+                if agree is None:
+                    raise
+                ok = False      # vote failure below; no collective was left half-done
+                self._after_oom()
+            if common(1.0 if ok and self.plan_note == "region" else 0.0, "min") < 0.5:
+                self._drop_step_plan()
+                return {}
+            info = self.ctx.plan_info()
+            items = self.ctx.plan_items()
+            T = max((max(a, b, c) for _, a, b, c in items), default=0) + 2
+            live = np.zeros(T, dtype=np.float64)
+            for size, a, b, c in items:
+                if b >= 0:
+                    live[a:b] += size
+            # the next recording's room: the pages not live once this plan's region
+            # is returned, less the page the pool keeps for unplanned allocations
+            limit = info["room_bytes"] * (1.0 - margin) - (64 << 20)
+            start_peak = float(live.max()) if T else 0.0
+            node_clock = probe["node_clock"]
+            issue = sorted(((c, gid, nb) for gid, (c, nb) in probe["issue"].items() if gid in cands))
+            moved = plan_window_moves(live, node_clock, issue, cands,
+                                      {g.gid: g.trigger for g in self.plan.groups}, limit)
+            # the live bytes bound the placement from below only: keep the longest
+            # prefix of the moves (in issue order) whose recorded step, with those
+            # destinations allocated at their new clocks, still places inside the
+            # room (the pool's own solver, lms_plan_solve)
+            sizes = [it[0] for it in items]
+            t0 = [it[1] for it in items]
+            t1 = [it[2] for it in items]
+            item_at = {a: i for i, a in enumerate(t0)}
+            # a move is modelled only if its destination is the allocation made at
+            # its issue clock (same bytes up to the pool's rounding)
+            moved = [m for m in moved if m[1] in item_at and 0 <= sizes[item_at[m[1]]] - m[3] < (4 << 20)]
 
-        def region_with(k):
-            tk = list(t0)
-            for gid, c1, c2, nb, _ in moved[:k]:
-                tk[item_at[c1]] = c2
-            return rt.plan_solve(sizes, tk, t1)[1]
+            def region_with(k):
+                tk = list(t0)
+                for gid, c1, c2, nb, _ in moved[:k]:
+                    tk[item_at[c1]] = c2
+                return rt.plan_solve(sizes, tk, t1)[1]
 
-        keep = len(moved)
-        if moved and region_with(keep) > limit:
-            lo, hi = 0, keep      # lo fits (the recorded plan), hi does not
-            while hi - lo > 1:
-                mid = (lo + hi) // 2
-                if region_with(mid) <= limit:
-                    lo = mid
-                else:
-                    hi = mid
-            keep = lo
-        # each rank models its own recorded step; the trial schedule is common
-        keep = int(common(float(keep), "min"))
+            keep = len(moved)
+            if moved and region_with(keep) > limit:
+                lo, hi = 0, keep      # lo fits (the recorded plan), hi does not
+                while hi - lo > 1:
+                    mid = (lo + hi) // 2
+                    if region_with(mid) <= limit:
+                        lo = mid
+                    else:
+                        hi = mid
+                keep = lo
+            # each rank models its own recorded step; the trial schedule is common
+            keep = int(common(float(keep), "min"))
+            if keep > 0 or attempt == 1 or common(float(len(moved)), "max") == 0:
+                break
         # the model predicts; replayed steps decide: re-record with the moves,
         # keep them if the placement fits at the physical-release lifetimes
         # (alpha 1: no block reused before its swap-out copy landed) and the
