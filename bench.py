@@ -613,6 +613,7 @@ def main():
     tuned = {}
     extra_warmup = 0
     prepared = None   # (cfg, plan, info) chosen by the joint search: timed as is
+    plan_state = {}   # the static plan as the timed steps ran it
 
     def run_timed(n_use, tune=False):
         """Warm-up + exactly ``args.steps`` timed swapped steps; None if the budget is hit."""
@@ -630,9 +631,16 @@ def main():
                 # record the chosen plan once more and time it: the timed run then
                 # replays exactly this recorded placement
                 final = lms.time_replay(xs, ys, 5, tune_agree)
+                if final is None:
+                    # this recording's placement did not fit (lifetimes vary with the
+                    # transfers' timing): record once more
+                    final = lms.time_replay(xs, ys, 5, tune_agree)
                 tuned = dict(prepared[2], reused=True, final_ms=final["ms"] if final else None,
                              final_spread_ms=final["spread"] if final else None)
                 prepared = None     # a retry (OOM) tunes afresh
+                if final is None:
+                    log("[bench] the tuned plan's recording did not fit twice: timing the untuned plan")
+                    return None
             elif tune:
                 tuned = lms.tune_windows(xs, ys, agree=tune_agree)
                 log(f"[bench] tune_windows: {tuned}")
@@ -651,12 +659,18 @@ def main():
                 if ctx.stats()["n_reclaims"] == r0:
                     break
             torch.cuda.synchronize(dev)
+            if tune and agree(1.0 if lms.plan_note == "region" else 0.0, "min") < 0.5:
+                # without its static plan the tuned step runs on the dynamic pool and
+                # moves pages every step: time the untuned plan instead
+                log(f"[bench] tuned plan has no static placement ({lms.plan_note}): timing the untuned plan")
+                return None
             ctx.trace_clear()
             ctx.reset_peaks()
             st0 = ctx.stats()
             clocks.start()
             ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps, tag="swapped")
             clk = clocks.stop()
+            plan_state.update(note=lms.plan_note, info=ctx.plan_info())
             return ms
         except RuntimeError as e:
             if not is_oom(e):
@@ -900,13 +914,13 @@ def main():
                  "device_peak_bytes": st1["device_peak"], "host_peak_bytes": st1["host_peak"],
                  "attempts": attempts, "capture_s": round(capture_s, 2),
                  "rewrite_s": round(plan.rewrite_seconds, 3), "bisect_s": round(bisect_s, 1),
-                 "graph_nodes": len(lms.graph.nodes), "static_plan": lms.plan_note, "tune_windows": tuned, "settling_warmup_steps": extra_warmup,
+                 "graph_nodes": len(lms.graph.nodes), "static_plan": plan_state.get("note"), "tune_windows": tuned, "settling_warmup_steps": extra_warmup,
                  "joint_n_tensors_ms": joint,
                  "timed_host_grows": st1["n_host_grow"] - st0["n_host_grow"],
                  "timed_host_grow_ms": round(st1["host_grow_ms"] - st0["host_grow_ms"], 1),
                  "timed_page_moves": st1["n_reclaims"] - st0["n_reclaims"],
                  "timed_pool_driver_ms": round(st1["pool_driver_ms"] - st0["pool_driver_ms"], 1),
-                 "plan_info": ctx.plan_info()},
+                 "plan_info": plan_state.get("info")},
         "host_link": {k: round(v, 2) for k, v in link.items()},
         "link_floor": link_floor(link, d2h_b / steps, h2d_b / steps, swap_ms / steps,
                                  noswap_ms / steps * bs / b0 if noswap_ms and b0 else None),
