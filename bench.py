@@ -670,7 +670,7 @@ def main():
             clocks.start()
             ms = timed(torch, dev, ws, lambda: lms.step(xs, ys), args.steps, tag="swapped")
             clk = clocks.stop()
-            plan_state.update(note=lms.plan_note, info=ctx.plan_info())
+            plan_state.update(note=lms.plan_note, info=ctx.plan_info(), items=ctx.plan_items())
             return ms
         except RuntimeError as e:
             if not is_oom(e):
@@ -944,7 +944,7 @@ def main():
         print(json.dumps(out), flush=True)
         try:   # the recorded step, for offline work on the plan solver
             with open(os.path.join(ROOT, "gpurun_out", f"plan_items_{args.arch}_{bs}.json"), "w") as fh:
-                json.dump({"items": ctx.plan_items(), "plan_info": ctx.plan_info()}, fh)
+                json.dump({"items": plan_state.get("items"), "plan_info": plan_state.get("info")}, fh)
         except OSError:
             pass
     if use_dist:
