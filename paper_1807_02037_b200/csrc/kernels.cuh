@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace lms {
@@ -483,55 +484,58 @@ __global__ void __launch_bounds__(256, 3) zvc_encode_kernel(const uint32_t* __re
         w16[r] = i < nwords ? __ldg(src + i) : 0u;
       }
     }
-    // per-tile statistics: nonzeros, and the top-byte ranges over all / nonzero words
-    uint32_t nnz = 0, mn_a = 127, mx_a = 0, or_a = 0, and_a = 1, mn_z = 127, mx_z = 0, or_z = 0, and_z = 1;
+    // per-tile statistics: nonzeros, and the top-byte ranges over all / nonzero
+    // words.  Zero words (and the zero padding past nvalid) have top byte 0, so
+    // the maximum and the sign OR over all words equal those over the nonzero
+    // ones; the nonzero words' sign AND is "no nonzero positive word"; only the
+    // all-words minimum and sign AND need the valid-word test (partial tiles).
+    uint32_t nnz = 0, mn_a = 127, mx = 0, orv = 0, andv = ~0u, mn_z = 127, posnz = 0;
+    auto tile_stats = [&](auto full) {
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const uint32_t v = w16[r];
-      nnz += v != 0;
-      if (kExp) {   // the top-byte ranges only matter when exponent planes are allowed
-        const uint32_t e7 = (v >> 24) & 0x7Fu, s = v >> 31;
-        if (uint32_t(r * 256 + threadIdx.x) < nvalid) {
-          mn_a = min(mn_a, e7);
-          mx_a = max(mx_a, e7);
-          or_a |= s;
-          and_a &= s;
-        }
-        if (v) {
-          mn_z = min(mn_z, e7);
-          mx_z = max(mx_z, e7);
-          or_z |= s;
-          and_z &= s;
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t v = w16[r];
+        nnz += v != 0;
+        if (kExp) {
+          const uint32_t e7 = (v >> 24) & 0x7Fu;
+          mx = max(mx, e7);
+          orv |= v;
+          mn_z = min(mn_z, v ? e7 : 127u);
+          posnz |= uint32_t(v - 1u < 0x7FFFFFFFu);
+          if (decltype(full)::value || uint32_t(r * 256 + threadIdx.x) < nvalid) {
+            mn_a = min(mn_a, e7);
+            andv &= v;
+          }
         }
       }
-    }
+    };
+    if (nvalid == uint32_t(kZvcTileWords)) tile_stats(std::true_type{});
+    else tile_stats(std::false_type{});
     nnz = __reduce_add_sync(0xffffffffu, nnz);
     if (kExp) {
       mn_a = __reduce_min_sync(0xffffffffu, mn_a);
-      mx_a = __reduce_max_sync(0xffffffffu, mx_a);
-      or_a = __reduce_or_sync(0xffffffffu, or_a);
-      and_a = __reduce_and_sync(0xffffffffu, and_a);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      orv = __reduce_or_sync(0xffffffffu, orv) >> 31;
+      andv = __reduce_and_sync(0xffffffffu, andv) >> 31;
       mn_z = __reduce_min_sync(0xffffffffu, mn_z);
-      mx_z = __reduce_max_sync(0xffffffffu, mx_z);
-      or_z = __reduce_or_sync(0xffffffffu, or_z);
-      and_z = __reduce_and_sync(0xffffffffu, and_z);
+      posnz = __reduce_or_sync(0xffffffffu, posnz);
     }
     if (lane == 0) {
-      red[warp][0] = nnz; red[warp][1] = mn_a; red[warp][2] = mx_a; red[warp][3] = or_a; red[warp][4] = and_a;
-      red[warp][5] = mn_z; red[warp][6] = mx_z; red[warp][7] = or_z; red[warp][8] = and_z;
+      red[warp][0] = nnz; red[warp][1] = mn_a; red[warp][2] = mx; red[warp][3] = orv; red[warp][4] = andv;
+      red[warp][5] = mn_z; red[warp][6] = posnz;
     }
     __syncthreads();
     // every thread takes the same decision from the 8 warps' partials (no
     // serial thread-0 step, no second barrier)
-    uint32_t z = 0, mna = 127, mxa = 0, ora = 0, anda = 1, mnz = 127, mxz = 0, orz = 0, andz = 1;
+    uint32_t z = 0, mna = 127, mxa = 0, ora = 0, anda = 1, mnz = 127, posz = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       z += red[k][0];
       if (kExp) {
         mna = min(mna, red[k][1]); mxa = max(mxa, red[k][2]); ora |= red[k][3]; anda &= red[k][4];
-        mnz = min(mnz, red[k][5]); mxz = max(mxz, red[k][6]); orz |= red[k][7]; andz &= red[k][8];
+        mnz = min(mnz, red[k][5]); posz |= red[k][6];
       }
     }
+    const uint32_t mxz = mxa, orz = ora, andz = posz ? 0u : 1u;
     uint32_t mode = kZRaw, bytes = zvc_pad16(4ull * nvalid), n = nvalid, k = 0, sp = 0, sc = 0, em = 0, hoff = 0;
     {
       const uint32_t bm = 512 + zvc_pad16(4ull * z);
