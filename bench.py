@@ -731,7 +731,10 @@ def main():
                                  branch_threshold=args.branch_threshold, fuse_swapins=args.fuse_swapins,
                                      swapin_fuse_distance=args.fuse_distance))
             try:
-                info = lms.tune_windows(xs, ys, agree=tune_agree)
+                # each candidate gets its base replay and at least one trial; no
+                # trial starts once the joint budget is spent
+                left = agree(args.tune_budget_s - (time.perf_counter() - t_joint), "min")
+                info = lms.tune_windows(xs, ys, agree=tune_agree, deadline_s=max(60.0, left))
             except RuntimeError as e:
                 if not is_oom(e) or use_dist:
                     raise

@@ -1061,7 +1061,8 @@ class LMS:
         return timings
 
     def tune_windows(self, x, y, lbs=(2, 3, 4, 5, 6, 8, 12, 16, 24, 32, 48, 64, 96), margin: float = 0.005,
-                     require_faster: bool = True, steps: int = 5, agree=None) -> dict:
+                     require_faster: bool = True, steps: int = 5, agree=None, max_trials: int = 4,
+                     deadline_s: float | None = None) -> dict:
         """Memory-aware control-op windows, one per swap-in (an extension: the
         paper leaves choosing lb open).  Every candidate control
         op comes from the reference's own strategy run with a wider window
@@ -1097,9 +1098,12 @@ class LMS:
         that hits the budget mid-step strands no peer in a collective; it keeps
         joining every ``agree`` with a failure vote instead.  The weights,
         buffers and optimizer state are restored at the end, so the replicas
-        stay identical."""
+        stay identical.
+
+        At most ``max_trials`` shrinking trials are timed, and none is started
+        past ``deadline_s`` seconds from the call (the slowest rank's clock)."""
         with self._local_replica(agree):
-            return self._tune_windows(x, y, lbs, margin, require_faster, steps, agree)
+            return self._tune_windows(x, y, lbs, margin, require_faster, steps, agree, max_trials, deadline_s)
 
     @contextlib.contextmanager
     def _local_replica(self, agree):
@@ -1130,7 +1134,8 @@ class LMS:
         with self._local_replica(agree):
             return self._timed_replay(x, y, steps, agree)
 
-    def _tune_windows(self, x, y, lbs, margin, require_faster, steps, agree) -> dict:
+    def _tune_windows(self, x, y, lbs, margin, require_faster, steps, agree, max_trials=4, deadline_s=None) -> dict:
+        t_call = time.perf_counter()
         from dataclasses import replace
         import numpy as np
         if not self.static_plan or self.plan is None:
@@ -1230,7 +1235,9 @@ class LMS:
         base_ms = base["ms"] if base else None
         trials, spreads = {}, {"base": base["spread"] if base else None}
         chosen = 0
-        while keep > 0:
+        while keep > 0 and len(trials) < max_trials:
+            if deadline_s is not None and common(time.perf_counter() - t_call, "max") > deadline_s:
+                break
             self._set_plan(retarget(orig, {m[0]: m[4] for m in moved[:keep]}))
             r = self._timed_replay(x, y, steps, agree)
             trials[keep] = r["ms"] if r else None
